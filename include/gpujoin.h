@@ -1,0 +1,167 @@
+/*
+ * gpujoin.h -- C ABI of the B200 epsilon self-join (arxiv 1809.09930).
+ *
+ * The library computes the distance-similarity self-join of PAPER.md §3.1
+ * (l.104-110): every ORDERED pair (a, b) of points of D with
+ * dist(a, b) = sqrt(sum_j (a(x_j) - b(x_j))^2) <= eps, the self pair (a, a)
+ * included (§5.2 l.800-802 counts it in |R|).  The test is evaluated in
+ * float64 as sum_j (a_j - b_j)^2 <= eps^2.
+ *
+ * The hot path is Algorithm 1 (§4.5 l.573-612): reorderVariance (§4.2),
+ * constructIndex over k < n dimensions (§3.2.1, §4.1), computeNumBatches
+ * (§3.2.2), SelfJoinKernel with SORTIDU (§4.3) and SHORTC (§4.4), and the
+ * entity partitioning of query points over GPUs (§6.2).
+ *
+ * Conventions for every entry point
+ *  - Return value: GJ_OK (0) on success, a negative GJ_ERR_* code otherwise;
+ *    gj_last_error() then returns a thread-local human-readable message.
+ *    No entry point aborts the process.
+ *  - "device pointer" = memory from cudaMalloc / torch CUDA tensors on the
+ *    current device; "host pointer" = ordinary or pinned host memory.
+ *  - All GPU work of an index is issued on the CUDA stream given in
+ *    gj_options.stream at build time (0 = legacy default stream).  Calls
+ *    marked [async] only enqueue work; others synchronise that stream.
+ *  - Point ids in results are the row numbers of the ORIGINAL input array
+ *    (0-based, uint32), independent of any internal reordering.
+ *  - Ownership: the caller owns every buffer it passes; the index owns its
+ *    own device memory until gj_free_index().
+ */
+#ifndef GPUJOIN_H
+#define GPUJOIN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GJ_API __attribute__((visibility("default")))
+#else
+#define GJ_API
+#endif
+
+#define GJ_OK 0
+#define GJ_ERR_INVALID -1   /* bad argument (null, size, k outside [1,n], eps <= 0 ...) */
+#define GJ_ERR_CUDA -2      /* a CUDA runtime call failed (message has the CUDA error) */
+#define GJ_ERR_OVERFLOW -3  /* linearised cell id needs >= 2^63: choose a smaller k (§4.1) */
+#define GJ_ERR_CAPACITY -4  /* result buffer too small; *n_pairs holds the required count */
+#define GJ_ERR_NOMEM -5     /* device or pinned allocation failed */
+
+typedef struct gj_index gj_index; /* opaque handle */
+
+/* Options of Algorithm 1.  Zero-initialise then set fields; gj_default_options fills them. */
+typedef struct {
+    int32_t reorder;     /* 1: REORDER dims by variance (§4.2); 0: index the first k dims */
+    int32_t sortidu;     /* 1: SORTIDU prune on the un-indexed dim u (§4.3)               */
+    int32_t shortc;      /* 1: SHORTC short-circuit of the distance sum (§4.4)            */
+    int32_t reserved0;
+    double sample_frac;  /* variance sample fraction (§4.2 "1% of |D|"), in (0,1]        */
+    uint64_t stream;     /* cudaStream_t the index issues its work on                     */
+} gj_options;
+
+/* Read-only description of a built index. */
+typedef struct {
+    int64_t n_points;     /* |D|                                                   */
+    int32_t dim;          /* n                                                     */
+    int32_t dim_pad;      /* n rounded up to a multiple of 4 (row stride, doubles) */
+    int32_t k;            /* indexed dims                                          */
+    int32_t u;            /* position (in reordered dims) of the SORTIDU dim       */
+    double eps;
+    int64_t n_cells;      /* |G|: non-empty cells (§5.6)                           */
+    int64_t n_adjacent;   /* sum over cells of non-empty adjacent cells            */
+    int64_t n_tiles;      /* query tiles (<= 128 queries of one cell each)         */
+    double est_candidates;/* sum over queries of candidates before SORTIDU         */
+    double build_ms;      /* device time of gj_build_index (CUDA events)           */
+} gj_info;
+
+/* Work counters of one join (gj_join_stats). */
+typedef struct {
+    int64_t cells;        /* (query, adjacent non-empty cell) visits                        */
+    int64_t tests;        /* candidate distance tests after SORTIDU                         */
+    int64_t dims;         /* dims evaluated with a per-dimension SHORTC check (algorithmic) */
+    int64_t pairs;        /* result pairs (ordered, self pairs included)                    */
+} gj_stats;
+
+GJ_API void gj_default_options(gj_options* opt);
+
+/* constructIndex (Alg. 1 l.581-582; §3.2.1, §4.1-4.3).
+ *  points : n_points x dim row-major float64, host OR device pointer (host
+ *           input is staged to the device inside the call).
+ *  eps    : > 0, search radius and grid cell edge length (§3.2.1 l.121).
+ *  k      : 1 <= k <= dim indexed dimensions (§4.1; the paper uses 2 <= k < n).
+ *  opt    : may be NULL (defaults: reorder=sortidu=shortc=1, sample_frac=0.01).
+ *  out    : receives the handle; free with gj_free_index.
+ * Errors: GJ_ERR_INVALID, GJ_ERR_OVERFLOW, GJ_ERR_CUDA, GJ_ERR_NOMEM.
+ * n_points must be < 2^32 - 1 (ids are uint32).  Synchronises the stream. */
+GJ_API int gj_build_index(const double* points, int64_t n_points, int32_t dim, double eps, int32_t k,
+                   const gj_options* opt, gj_index** out);
+
+GJ_API int gj_index_info(const gj_index* idx, gj_info* info);
+
+/* Dimension order chosen by REORDER: order[t] = original dim at position t. */
+GJ_API int gj_dim_order(const gj_index* idx, int32_t* order, int32_t cap);
+
+/* Device pointer to the index's reordered, cell-sorted point array
+ * (n_points x dim_pad float64) and its sorted-position -> original-id map. */
+GJ_API int gj_device_arrays(const gj_index* idx, const double** points_sorted, const uint32_t** orig_id);
+
+/* Result-size estimator (§3.2.2 l.199): runs the join in count-only mode on
+ * every round(1/frac)-th query tile of this rank's share and scales by the
+ * sampled query fraction.  Returns estimated pairs of this rank's share. */
+GJ_API int gj_estimate(gj_index* idx, double frac, int32_t rank, int32_t world, int64_t* est_pairs);
+
+/* computeNumBatches (§3.2.2 l.199-200): n_b = max(3, ceil(est / batch_size)). */
+GJ_API int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size);
+
+/* selfJoinKernel for one batch (Alg. 1 l.586) [async].
+ *  Processes batch `batch` of `n_batches` of rank `rank`'s share of the
+ *  query tiles (entity partitioning §6.2: tile position j in the index's
+ *  heaviest-first order belongs to rank j mod world; batch = (j div world)
+ *  mod n_batches).  Appends ordered pairs (query_id, neighbour_id) as uint32
+ *  pairs to out_pairs (device, capacity pairs) at positions obtained from the
+ *  device counter *d_count (uint64, device pointer; caller zeroes it before
+ *  the first batch that shares the buffer).  Pairs past capacity are counted
+ *  but not written: after the stream completes, *d_count > capacity means the
+ *  batch must be re-run with a larger buffer.  Pair order is unspecified. */
+GJ_API int gj_self_join_async(gj_index* idx, uint32_t* out_pairs, int64_t capacity, uint64_t* d_count,
+                       int32_t batch, int32_t n_batches, int32_t rank, int32_t world);
+
+/* Same, count only (no pair payload written) [async]. */
+GJ_API int gj_self_join_count_async(gj_index* idx, uint64_t* d_count, int32_t batch, int32_t n_batches,
+                             int32_t rank, int32_t world);
+
+/* Convenience: whole share of `rank` into a device buffer, synchronous.
+ * On GJ_ERR_CAPACITY *n_pairs holds the required capacity. */
+GJ_API int gj_self_join(gj_index* idx, uint32_t* out_pairs, int64_t capacity, int32_t rank, int32_t world,
+                 int64_t* n_pairs);
+
+/* The full GPU-Join pipeline of Alg. 1 with Fig. 4's overlap: estimator,
+ * n_b = max(3, ceil(est/batch_size)) batches on 3 streams with 3 device
+ * result buffers, device->host drains of each batch overlapping the next
+ * batch's kernel, into the HOST buffer out_pairs (capacity pairs).  If
+ * out_pairs is pinned the drains land in it directly, otherwise through 3
+ * pinned staging buffers.  batch_size <= 0 selects b_s = 1e8 (§3.2.2).
+ * On GJ_ERR_CAPACITY *n_pairs holds the required capacity. */
+GJ_API int gj_self_join_host(gj_index* idx, uint32_t* out_pairs, int64_t capacity, int32_t rank,
+                      int32_t world, int64_t batch_size, int64_t* n_pairs, int32_t* n_batches_out);
+
+/* Work counters of rank's share (cells visited, SORTIDU-window tests,
+ * algorithmic SHORTC dims, pairs).  Synchronous; slower than the join. */
+GJ_API int gj_join_stats(gj_index* idx, int32_t rank, int32_t world, gj_stats* st);
+
+/* constructNeighborTable (Alg. 1 l.587): sort n_pairs device pairs by
+ * (query, neighbour) in place and write the CSR offsets (n_points + 1
+ * uint64, device) of each query's neighbour run.  Synchronous. */
+GJ_API int gj_neighbor_table(gj_index* idx, uint32_t* pairs, int64_t n_pairs, uint64_t* offsets);
+
+GJ_API void gj_free_index(gj_index* idx);
+GJ_API const char* gj_last_error(void);
+GJ_API int32_t gj_abi_version(void);
+/* Number of CUDA kernels this library has launched in this process. */
+GJ_API int64_t gj_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPUJOIN_H */

@@ -1,0 +1,435 @@
+// constructIndex on the device (Alg. 1 l.581-582).
+//
+//  1. per-dim min/max over D and variance over the 1% sample (§4.2 l.498)
+//  2. REORDER permutation by non-increasing variance, grid geometry over the
+//     first k reordered dims (§4.1 l.252), overflow check of the linear id
+//  3. per point: linearised cell id (§3.2.1 l.122, row-major) and the SORTIDU
+//     key of the un-indexed dim u (§4.3 l.514)
+//  4. stable device radix sort by u, then by cell id -> points grouped by cell,
+//     u-sorted within each cell (§3.2.1 "lookup array"; §4.3 sort)
+//  5. gather of the reordered, sorted point array (row stride n_pad)
+//  6. non-empty cell array (ids + starts), |G| (§3.2.1 l.119, l.122)
+//  7. adjacent non-empty cells of every cell: 3^k offsets located by binary
+//     search (§3.2.1 l.185, §5.6 l.896), CSR
+//  8. query tiles (<= 128 queries of one cell) with their candidate count,
+//     ordered heaviest first for load balance (§6.2 entity partitioning).
+//
+// Readings: R2 cell_j = floor(x_j/eps) - floor(min_j/eps);
+// R6 sample = every round(1/f)-th point, unbiased variance, ties -> lower dim;
+// R7 u = position k if k < n else 0; R9 first indexed dim most significant.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "gj_internal.cuh"
+
+namespace gj {
+namespace {
+
+enum ColMode { kMinMax = 0, kSum = 1, kSqDev = 2 };
+
+// Column reduction over rows r = i * rstride, i in [0, m).  Block size is a
+// multiple of n so each thread owns one column; partials are [block][n]
+// (and [block][n] for the max in kMinMax mode at part2).
+__global__ void k_col_reduce(const double* __restrict__ X, int64_t m, int64_t rstride, int n, int mode,
+                             const double* __restrict__ mean, double* __restrict__ part,
+                             double* __restrict__ part2) {
+    extern __shared__ double sh[];
+    const int rpb = blockDim.x / n;
+    const int j = threadIdx.x % n, rl = threadIdx.x / n;
+    double a = mode == kMinMax ? INFINITY : 0.0, b = -INFINITY;
+    const double mu = mode == kSqDev ? mean[j] : 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * rpb + rl; i < m; i += (int64_t)gridDim.x * rpb) {
+        double x = X[i * rstride * n + j];
+        if (mode == kMinMax) {
+            a = fmin(a, x);
+            b = fmax(b, x);
+        } else if (mode == kSum) {
+            a += x;
+        } else {
+            double d = x - mu;
+            a += d * d;
+        }
+    }
+    double* sa = sh;
+    double* sb = sh + blockDim.x;
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    if (rl == 0) {
+        for (int r = 1; r < rpb; ++r) {
+            if (mode == kMinMax) {
+                a = fmin(a, sa[r * n + j]);
+                b = fmax(b, sb[r * n + j]);
+            } else {
+                a += sa[r * n + j];
+            }
+        }
+        part[(int64_t)blockIdx.x * n + j] = a;
+        if (mode == kMinMax) part2[(int64_t)blockIdx.x * n + j] = b;
+    }
+}
+
+// Sequential (deterministic) reduction of the block partials; one thread per column.
+__global__ void k_col_final(const double* __restrict__ part, const double* __restrict__ part2, int nb, int n,
+                            int mode, int64_t m, double* __restrict__ outa, double* __restrict__ outb) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double a = mode == kMinMax ? INFINITY : 0.0, b = -INFINITY;
+    for (int i = 0; i < nb; ++i) {
+        if (mode == kMinMax) {
+            a = fmin(a, part[(int64_t)i * n + j]);
+            b = fmax(b, part2[(int64_t)i * n + j]);
+        } else {
+            a += part[(int64_t)i * n + j];
+        }
+    }
+    if (mode == kMinMax) {
+        outa[j] = a;
+        outb[j] = b;
+    } else if (mode == kSum) {
+        outa[j] = a / (double)m;          // sample mean
+    } else {
+        outa[j] = m > 1 ? a / (double)(m - 1) : 0.0;   // unbiased sample variance
+    }
+}
+
+// REORDER permutation + grid geometry (single block).
+__global__ void k_meta(Meta* meta, int n, int k, double eps, int reorder) {
+    const int t = threadIdx.x;
+    if (t < n) {
+        int rank = t;
+        if (reorder) {
+            double v = meta->var[t];
+            rank = 0;
+            for (int i = 0; i < n; ++i) {
+                double w = meta->var[i];
+                rank += (w > v) || (w == v && i < t);
+            }
+        }
+        meta->order[rank] = t;
+    }
+    __syncthreads();
+    if (t == 0) {
+        int overflow = 0;
+        double prod = 1.0;
+        for (int d = 0; d < k; ++d) {
+            int o = meta->order[d];
+            double fb = floor(meta->mins[o] / eps), fm = floor(meta->maxs[o] / eps);
+            if (!(fabs(fb) < 4.0e18) || !(fabs(fm) < 4.0e18)) overflow = 1;
+            int64_t b = overflow ? 0 : (int64_t)fb;
+            int64_t w = overflow ? 1 : (int64_t)fm - b + 1;
+            meta->base[d] = b;
+            meta->width[d] = w;
+            prod *= (double)w;
+        }
+        if (prod >= 9.2e18) overflow = 1;
+        uint64_t s = 1;
+        for (int d = k - 1; d >= 0; --d) {
+            meta->stride[d] = s;
+            s *= (uint64_t)meta->width[d];
+        }
+        meta->overflow = overflow;
+    }
+}
+
+__device__ __forceinline__ uint64_t order_key(double x) {
+    uint64_t b = (uint64_t)__double_as_longlong(x + 0.0);   // -0.0 -> +0.0
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_cell_keys(const double* __restrict__ X, int64_t N, int n, int k, int u, double eps,
+                            const Meta* __restrict__ meta, uint64_t* __restrict__ cellkey,
+                            uint64_t* __restrict__ ukey, uint32_t* __restrict__ idx) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double* x = X + i * n;
+    uint64_t lin = 0;
+    for (int d = 0; d < k; ++d) {
+        int o = meta->order[d];
+        int64_t c = (int64_t)floor(x[o] / eps) - meta->base[d];
+        lin += (uint64_t)c * meta->stride[d];
+    }
+    cellkey[i] = lin;
+    ukey[i] = order_key(x[meta->order[u]]);
+    idx[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx, int64_t N,
+                             uint64_t* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) dst[i] = src[idx[i]];
+}
+
+// pts[p][t] = X[idx[p]][order[t]] (0 for t >= n); one thread per output element.
+__global__ void k_gather_points(const double* __restrict__ X, const uint32_t* __restrict__ idx, int64_t N,
+                                int n, int n_pad, const Meta* __restrict__ meta, double* __restrict__ pts) {
+    __shared__ int ord[kMaxDim];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) ord[t] = meta->order[t];
+    __syncthreads();
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * n_pad) return;
+    int64_t p = e / n_pad;
+    int t = (int)(e - p * n_pad);
+    pts[e] = t < n ? X[(int64_t)idx[p] * n + ord[t]] : 0.0;
+}
+
+__global__ void k_heads(const uint64_t* __restrict__ key, int64_t N, uint32_t* __restrict__ head) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < N) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1u : 0u;
+}
+
+__global__ void k_cells(const uint64_t* __restrict__ key, const uint32_t* __restrict__ head,
+                        const uint32_t* __restrict__ pos, int64_t N, uint64_t* __restrict__ cell_id,
+                        uint32_t* __restrict__ cell_start, int64_t G) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < N && head[p]) {
+        cell_id[pos[p]] = key[p];
+        cell_start[pos[p]] = (uint32_t)p;
+    }
+    if (p == 0) cell_start[G] = (uint32_t)N;
+}
+
+// Adjacent non-empty cells (getAdjCells): one warp per cell, lanes split the
+// 3^k offsets (row-major over {-1,0,1}^k), each located by binary search in
+// the sorted id array.  FILL=false: counts + candidate sums; FILL=true: CSR.
+template <bool FILL>
+__global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t* __restrict__ cell_start,
+                           int64_t G, int k, const Meta* __restrict__ meta, uint32_t* __restrict__ cnt,
+                           uint64_t* __restrict__ cand, const uint32_t* __restrict__ off,
+                           uint32_t* __restrict__ nbr) {
+    __shared__ int64_t s_w[kMaxK];
+    __shared__ uint64_t s_s[kMaxK];
+    if (threadIdx.x < k) {
+        s_w[threadIdx.x] = meta->width[threadIdx.x];
+        s_s[threadIdx.x] = meta->stride[threadIdx.x];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= G) return;
+    const uint64_t lin = cell_id[g];
+    int64_t c[kMaxK];
+    for (int d = 0; d < k; ++d) c[d] = (int64_t)((lin / s_s[d]) % (uint64_t)s_w[d]);
+    int64_t total = 1;
+    for (int d = 0; d < k; ++d) total *= 3;
+    const uint64_t lo_id = cell_id[0], hi_id = cell_id[G - 1];
+    uint32_t found = 0, wpos = FILL ? off[g] : 0;
+    uint64_t csum = 0;
+    for (int64_t o0 = 0; o0 < total; o0 += 32) {
+        int64_t o = o0 + lane;
+        bool ok = o < total;
+        int64_t hit = -1;
+        if (ok) {
+            int64_t r = o;
+            uint64_t nl = 0;
+            for (int d = k - 1; d >= 0; --d) {
+                int64_t cd = c[d] + (r % 3) - 1;
+                r /= 3;
+                if (cd < 0 || cd >= s_w[d]) ok = false;
+                nl += (uint64_t)cd * s_s[d];
+            }
+            if (ok && nl >= lo_id && nl <= hi_id) {
+                int64_t lo = 0, hi = G;
+                while (lo < hi) {
+                    int64_t mid = (lo + hi) >> 1;
+                    if (cell_id[mid] < nl) lo = mid + 1; else hi = mid;
+                }
+                if (lo < G && cell_id[lo] == nl) hit = lo;
+            }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, hit >= 0);
+        if (FILL) {
+            if (hit >= 0) nbr[wpos + __popc(m & ((1u << lane) - 1u))] = (uint32_t)hit;
+            wpos += __popc(m);
+        } else {
+            found += __popc(m);
+            if (hit >= 0) csum += cell_start[hit + 1] - cell_start[hit];
+        }
+    }
+    if (!FILL) {
+#pragma unroll
+        for (int s = 16; s; s >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, s);
+        if (lane == 0) {
+            cnt[g] = found;
+            cand[g] = csum;
+        }
+    }
+}
+
+__global__ void k_tile_count(const uint32_t* __restrict__ cell_start, int64_t G, uint32_t* __restrict__ nt) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < G) nt[g] = (cell_start[g + 1] - cell_start[g] + kTileQ - 1) / kTileQ;
+}
+
+__global__ void k_tile_fill(const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ toff,
+                            const uint64_t* __restrict__ cand, int64_t G, uint32_t* __restrict__ tile_cell,
+                            uint32_t* __restrict__ tile_q0, uint64_t* __restrict__ tile_work,
+                            uint64_t* __restrict__ sort_key, uint32_t* __restrict__ sort_val,
+                            unsigned long long* __restrict__ total) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    uint32_t a = cell_start[g], b = cell_start[g + 1];
+    uint32_t t = toff[g];
+    for (uint32_t q = a; q < b; q += kTileQ, ++t) {
+        uint32_t nq = min((uint32_t)kTileQ, b - q);
+        uint64_t w = (uint64_t)nq * cand[g];
+        tile_cell[t] = (uint32_t)g;
+        tile_q0[t] = q;
+        tile_work[t] = w;
+        sort_key[t] = ~w;   // descending work
+        sort_val[t] = t;
+    }
+    atomicAdd(total, (unsigned long long)((uint64_t)(b - a) * cand[g]));
+}
+
+int col_reduce(const double* X, int64_t m, int64_t rstride, int n, int mode, const double* mean, double* outa,
+               double* outb, cudaStream_t s) {
+    int rpb = std::max(1, 256 / n);
+    int bs = rpb * n;
+    int64_t need = (m + rpb - 1) / rpb;
+    int nb = (int)std::max<int64_t>(1, std::min<int64_t>(need, 592));
+    double* part = nullptr;
+    GJ_CUDA(cudaMallocAsync(&part, 2 * (size_t)nb * n * sizeof(double), s));
+    k_col_reduce<<<nb, bs, 2 * bs * sizeof(double), s>>>(X, m, rstride, n, mode, mean, part, part + (size_t)nb * n); count_launch();
+    k_col_final<<<(n + 127) / 128, 128, 0, s>>>(part, part + (size_t)nb * n, nb, n, mode, m, outa, outb); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    GJ_CUDA(cudaFreeAsync(part, s));
+    return GJ_OK;
+}
+
+inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+}  // namespace
+
+int build_index(Index* ix, const double* X) {
+    cudaStream_t s = ix->stream;
+    const int64_t N = ix->N;
+    const int n = ix->n, k = ix->k;
+    int rc;
+    cudaEvent_t ev0, ev1;
+    GJ_CUDA(cudaEventCreate(&ev0));
+    GJ_CUDA(cudaEventCreate(&ev1));
+    GJ_CUDA(cudaEventRecord(ev0, s));
+
+    GJ_CUDA(cudaMallocAsync(&ix->meta, sizeof(Meta), s));
+    GJ_CUDA(cudaMemsetAsync(ix->meta, 0, sizeof(Meta), s));
+    Meta* M = ix->meta;
+    // 1. min/max over D, variance over the sample
+    if ((rc = col_reduce(X, N, 1, n, kMinMax, nullptr, M->mins, M->maxs, s))) return rc;
+    const int64_t step = std::max<int64_t>(1, (int64_t)llround(1.0 / ix->opt.sample_frac));
+    const int64_t m = (N + step - 1) / step;
+    double* mean = nullptr;
+    GJ_CUDA(cudaMallocAsync(&mean, n * sizeof(double), s));
+    if ((rc = col_reduce(X, m, step, n, kSum, nullptr, mean, nullptr, s))) return rc;
+    if ((rc = col_reduce(X, m, step, n, kSqDev, mean, M->var, nullptr, s))) return rc;
+    GJ_CUDA(cudaFreeAsync(mean, s));
+    // 2. permutation + geometry
+    k_meta<<<1, 128, 0, s>>>(M, n, k, ix->eps, ix->opt.reorder); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    GJ_CUDA(cudaMemcpyAsync(&ix->h_meta, M, sizeof(Meta), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaStreamSynchronize(s));
+    if (ix->h_meta.overflow) {
+        set_error("linearized cell id needs >= 2^63 cells (prod of per-dim widths); choose a smaller k");
+        return GJ_ERR_OVERFLOW;
+    }
+    // 3. keys
+    uint64_t *cellkey = nullptr, *ukey = nullptr, *tmp64 = nullptr;
+    uint32_t* idx = nullptr;
+    GJ_CUDA(cudaMallocAsync(&cellkey, N * sizeof(uint64_t), s));
+    GJ_CUDA(cudaMallocAsync(&ukey, N * sizeof(uint64_t), s));
+    GJ_CUDA(cudaMallocAsync(&tmp64, N * sizeof(uint64_t), s));
+    GJ_CUDA(cudaMallocAsync(&idx, N * sizeof(uint32_t), s));
+    k_cell_keys<<<blocks_for(N, 256), 256, 0, s>>>(X, N, n, k, ix->u, ix->eps, M, cellkey, ukey, idx); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    // 4. stable sort by u, then by cell id
+    uint64_t vb = 0;
+    if (ix->opt.sortidu) {
+        if ((rc = varying_bits_u64(ukey, N, &vb, s))) return rc;
+        if ((rc = radix_sort_u64(ukey, idx, N, vb, s))) return rc;
+    }
+    k_gather_u64<<<blocks_for(N, 256), 256, 0, s>>>(cellkey, idx, N, tmp64); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    if ((rc = varying_bits_u64(tmp64, N, &vb, s))) return rc;
+    if ((rc = radix_sort_u64(tmp64, idx, N, vb, s))) return rc;
+    // 5. sorted, reordered point array
+    GJ_CUDA(cudaMallocAsync(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
+    GJ_CUDA(cudaMallocAsync(&ix->orig, N * sizeof(uint32_t), s));
+    k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts); count_launch();
+    GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    // 6. non-empty cells
+    uint32_t *head = nullptr, *pos = nullptr, *d_tot = nullptr;
+    GJ_CUDA(cudaMallocAsync(&head, N * sizeof(uint32_t), s));
+    GJ_CUDA(cudaMallocAsync(&pos, N * sizeof(uint32_t), s));
+    GJ_CUDA(cudaMallocAsync(&d_tot, 4 * sizeof(uint32_t), s));
+    k_heads<<<blocks_for(N, 256), 256, 0, s>>>(tmp64, N, head); count_launch();
+    if ((rc = scan_u32(head, pos, N, d_tot, s))) return rc;
+    uint32_t h_tot = 0;
+    GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaStreamSynchronize(s));
+    const int64_t G = h_tot;
+    ix->G = G;
+    GJ_CUDA(cudaMallocAsync(&ix->cell_id, G * sizeof(uint64_t), s));
+    GJ_CUDA(cudaMallocAsync(&ix->cell_start, (G + 1) * sizeof(uint32_t), s));
+    k_cells<<<blocks_for(N, 256), 256, 0, s>>>(tmp64, head, pos, N, ix->cell_id, ix->cell_start, G); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    // 7. adjacent non-empty cells
+    uint32_t* cnt = head;               // reuse (G <= N)
+    uint64_t* cand = tmp64;             // reuse: tmp64 no longer needed
+    GJ_CUDA(cudaMallocAsync(&ix->nbr_off, (G + 1) * sizeof(uint32_t), s));
+    k_adjacent<false><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, cnt, cand,
+                                                             nullptr, nullptr); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    if ((rc = scan_u32(cnt, ix->nbr_off, G, d_tot, s))) return rc;
+    GJ_CUDA(cudaMemcpyAsync(ix->nbr_off + G, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaStreamSynchronize(s));
+    ix->A = h_tot;
+    GJ_CUDA(cudaMallocAsync(&ix->nbr, std::max<int64_t>(1, ix->A) * sizeof(uint32_t), s));
+    k_adjacent<true><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, nullptr,
+                                                            nullptr, ix->nbr_off, ix->nbr); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    // 8. tiles, heaviest first
+    k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, pos); count_launch();
+    if ((rc = scan_u32(pos, pos, G, d_tot, s))) return rc;
+    GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaStreamSynchronize(s));
+    const int64_t T = h_tot;
+    ix->T = T;
+    GJ_CUDA(cudaMallocAsync(&ix->tile_cell, T * sizeof(uint32_t), s));
+    GJ_CUDA(cudaMallocAsync(&ix->tile_q0, T * sizeof(uint32_t), s));
+    GJ_CUDA(cudaMallocAsync(&ix->tile_order, T * sizeof(uint32_t), s));
+    GJ_CUDA(cudaMallocAsync(&ix->tile_work, T * sizeof(uint64_t), s));
+    uint64_t* skey = ukey;              // reuse (T <= N)
+    unsigned long long* d_total = nullptr;
+    GJ_CUDA(cudaMallocAsync(&d_total, sizeof(*d_total), s));
+    GJ_CUDA(cudaMemsetAsync(d_total, 0, sizeof(*d_total), s));
+    k_tile_fill<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, pos, cand, G, ix->tile_cell, ix->tile_q0,
+                                                   ix->tile_work, skey, ix->tile_order, d_total); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    if ((rc = varying_bits_u64(skey, T, &vb, s))) return rc;
+    if ((rc = radix_sort_u64(skey, ix->tile_order, T, vb, s))) return rc;
+    unsigned long long h_total = 0;
+    GJ_CUDA(cudaMemcpyAsync(&h_total, d_total, sizeof(h_total), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaMallocAsync(&ix->scratch_count, 8 * sizeof(uint64_t), s));
+    GJ_CUDA(cudaFreeAsync(d_total, s));
+    GJ_CUDA(cudaFreeAsync(cellkey, s));
+    GJ_CUDA(cudaFreeAsync(ukey, s));
+    GJ_CUDA(cudaFreeAsync(tmp64, s));
+    GJ_CUDA(cudaFreeAsync(idx, s));
+    GJ_CUDA(cudaFreeAsync(head, s));
+    GJ_CUDA(cudaFreeAsync(pos, s));
+    GJ_CUDA(cudaFreeAsync(d_tot, s));
+    GJ_CUDA(cudaEventRecord(ev1, s));
+    GJ_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    GJ_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    ix->build_ms = ms;
+    ix->est_candidates = (double)h_total;
+    return GJ_OK;
+}
+
+}  // namespace gj

@@ -1,0 +1,99 @@
+// Internal declarations shared by the CUDA translation units of libgpujoin.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/gpujoin.h"
+
+namespace gj {
+
+constexpr int kTileQ = 128;          // queries per tile = threads per join CTA
+constexpr int kMaxDim = 128;         // largest supported n (query dims live in registers)
+
+void set_error(const std::string& msg);
+
+// Kernels launched by this library (bench.py reports it as gpu_launches).
+extern std::atomic<long long> g_launches;
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+#define GJ_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            ::gj::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));           \
+            return GJ_ERR_CUDA;                                                              \
+        }                                                                                    \
+    } while (0)
+
+// Device-resident metadata written by the index-build kernels.
+struct Meta {
+    int32_t order[kMaxDim];      // REORDER permutation: position t <- original dim
+    double mins[kMaxDim];
+    double maxs[kMaxDim];
+    double var[kMaxDim];
+    int64_t base[16];                // per indexed dim: floor(min/eps)
+    int64_t width[16];               // cells per indexed dim
+    uint64_t stride[16];             // row-major strides of the linear id
+    int32_t overflow;                // 1 if prod(width) >= 2^63
+    int32_t pad_;
+};
+constexpr int kMaxK = 16;
+
+struct Index {
+    int64_t N = 0;
+    int32_t n = 0, n_pad = 0, k = 0, u = 0;
+    double eps = 0, eps2 = 0;
+    gj_options opt{};
+    cudaStream_t stream = 0;
+    // device arrays
+    double* pts = nullptr;           // [N][n_pad] reordered dims, sorted by (cell, u)
+    uint32_t* orig = nullptr;        // [N] sorted position -> original id
+    uint64_t* cell_id = nullptr;     // [G] sorted non-empty linear ids
+    uint32_t* cell_start = nullptr;  // [G+1]
+    uint32_t* nbr_off = nullptr;     // [G+1]
+    uint32_t* nbr = nullptr;         // [A] adjacent non-empty cells (offset order)
+    uint32_t* tile_cell = nullptr;   // [T]
+    uint32_t* tile_q0 = nullptr;     // [T]
+    uint32_t* tile_order = nullptr;  // [T] tiles, heaviest estimated work first
+    uint64_t* tile_work = nullptr;   // [T] queries * candidates (pre-SORTIDU)
+    Meta* meta = nullptr;            // device
+    uint64_t* scratch_count = nullptr;   // [4] device counters
+    Meta h_meta{};                   // host copy
+    int64_t G = 0, A = 0, T = 0;
+    double est_candidates = 0, build_ms = 0;
+    // result pipeline resources (lazily created)
+    cudaStream_t pipe_stream[3] = {0, 0, 0};
+    cudaEvent_t pipe_event[3] = {0, 0, 0};
+};
+
+// ---- radix sort / scan (gj_radix.cu) ----
+// Exclusive scan of n uint32 -> uint32 (out may alias in); total returned via d_total (device).
+int scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* d_total, cudaStream_t s);
+// Stable LSD radix sort of (key, val) pairs on the key bits set in `bits_mask`.
+// keys/vals are sorted in place (double-buffered internally).
+int radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, uint64_t bits_mask, cudaStream_t s);
+// OR over i of (keys[i] ^ keys[0]) -> host.
+int varying_bits_u64(const uint64_t* keys, int64_t n, uint64_t* h_out, cudaStream_t s);
+
+// ---- index build (gj_index.cu) ----
+int build_index(Index* ix, const double* d_points);
+
+// ---- join (gj_join.cu) ----
+enum JoinMode { kEmit = 0, kCount = 1, kStats = 2 };
+struct JoinArgs {
+    uint32_t* out;            // [cap][2]
+    uint64_t cap;
+    uint64_t* count;          // device counter(s); kStats: [4] = cells, tests, dims, pairs
+    int64_t first;            // first tile position j
+    int64_t step;             // tile positions j = first + step * m
+    int64_t n_tiles;          // number of m values
+};
+int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+// Number of tile positions for (rank, world, batch, n_batches); sets first/step.
+void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
+                 JoinArgs* a);
+
+}  // namespace gj

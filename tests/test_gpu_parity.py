@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA self-join (through the C ABI) against the CPU oracles.
+
+Bar (north_star): the GPU pair set equals the brute-force oracle's exactly,
+apart from pairs with |d^2 - eps^2| <= 1e-12 eps^2 ("ambiguous"), which may
+fall either way and are counted.  Integer work counters (cells, SORTIDU tests,
+SHORTC dims, pairs) must equal the Algorithm-1 oracle's exactly.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import brute, grid
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def gpu_pairs(D, eps, k, world=1, rank=None, **flags):
+    from paper_1809_09930_b200 import Index
+    ix = Index(torch.from_numpy(np.ascontiguousarray(D)).cuda(), eps, k, **flags)
+    ranks = range(world) if rank is None else [rank]
+    res = []
+    for r in ranks:
+        cap = max(ix.estimate(1.0, r, world) + 1024, 1024)
+        out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+        n = ix.self_join(out, r, world)
+        res.append(out[:n].cpu().numpy().view(np.uint32).astype(np.int64))
+    return np.concatenate(res), ix
+
+
+def check(D, eps, got):
+    sure, amb = brute.self_join(D, eps)
+    S = {tuple(r) for r in sure.tolist()}
+    A = {tuple(r) for r in amb.tolist()}
+    G = {tuple(r) for r in got.tolist()}
+    assert len(G) == len(got), "duplicate pairs emitted"
+    missing, extra = S - G, G - S - A
+    assert not missing and not extra, (len(missing), len(extra), list(missing)[:5], list(extra)[:5])
+    return len(A), len(G & A)
+
+
+SMALL = [  # (generator, |D|, n, eps, k)
+    ("uniform", 2000, 16, 0.96, 6),       # BASELINE configs[0] (~8 neighbours/point)
+    ("exponential", 3000, 16, 0.04, 6),
+    ("exponential", 2500, 32, 0.08, 6),
+    ("exponential", 1500, 64, 0.16, 6),
+    ("uniform", 3000, 3, 0.02, 2),
+    ("uniform", 1000, 90, 1.2, 8),
+    ("exponential", 1777, 18, 0.05, 1),   # ragged tiles, k = 1
+    ("exponential", 900, 5, 0.05, 5),     # k = n (u = dim 1)
+]
+
+
+@pytest.mark.parametrize("gen,count,dims,eps,k", SMALL)
+def test_pairs_equal_brute_force(gen, count, dims, eps, k):
+    D = synth.make(gen, count, dims, seed=count * 7 + dims)
+    got, ix = gpu_pairs(D, eps, k)
+    amb, amb_in = check(D, eps, got)
+    assert len(got) > count                       # real neighbours, not just self pairs
+
+
+@pytest.mark.parametrize("reorder,sortidu,shortc", [(r, s, c) for r in (0, 1) for s in (0, 1) for c in (0, 1)])
+def test_every_flag_combination(reorder, sortidu, shortc):
+    D = synth.exponential(2200, 24, seed=5)
+    got, _ = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc)
+    check(D, 0.07, got)
+
+
+def test_lattice_exact_boundaries_are_inclusive():
+    # integer lattice, eps = 1 exactly: axis neighbours sit exactly on the
+    # boundary (d^2 == eps^2 computed exactly) and the paper's <= includes them.
+    D = synth.lattice(6, 3)
+    got, _ = gpu_pairs(D, 1.0, 2)
+    sure, amb = brute.self_join(D, 1.0)
+    G = {tuple(r) for r in got.tolist()}
+    assert {tuple(r) for r in sure.tolist()} | {tuple(r) for r in amb.tolist()} == G
+    assert len(G) == 216 + 3 * 2 * 5 * 36
+
+
+def test_degenerate_inputs():
+    # one point; all points identical (one cell, every pair at distance 0);
+    # points with a constant dimension; negative coordinates.
+    got, _ = gpu_pairs(np.array([[0.5, 0.25, 0.125]]), 0.1, 2)
+    assert got.tolist() == [[0, 0]]
+    D = np.tile(np.array([[0.3, 0.3, 0.3, 0.3]]), (300, 1))
+    got, ix = gpu_pairs(D, 0.01, 3)
+    assert len(got) == 300 * 300 and ix.info().n_cells == 1
+    D = synth.uniform(1200, 6, seed=2) - 0.5
+    D[:, 2] = 0.0
+    got, _ = gpu_pairs(D, 0.2, 3)
+    check(D, 0.2, got)
+
+
+def test_index_structure_matches_algorithm1_oracle():
+    # distinct per-dim scales so the REORDER order has no near-ties
+    D = synth.uniform(2500, 10, seed=8) * np.linspace(1.0, 0.1, 10)[::-1]
+    eps, k = 0.06, 4
+    from paper_1809_09930_b200 import Index
+    ix = Index(torch.from_numpy(D).cuda(), eps, k, sample_frac=0.01)
+    Dr, order = grid.reorder_variance(D, 0.01)
+    assert ix.dim_order().tolist() == order.tolist()
+    G = grid.construct_index(Dr, eps, k)
+    info = ix.info()
+    assert info.n_cells == len(G["cell_ids"]) and info.u == G["u"]
+    # sorted point order: same (cell, u, id) order as the oracle's lookup array
+    pts, orig = ix.device_arrays()
+    assert orig.cpu().numpy().tolist() == G["order"].tolist()
+    # the reordered, sorted point array holds exactly the oracle's rows
+    ref = Dr[G["order"]]
+    assert np.array_equal(pts[:, :D.shape[1]].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("gen,count,dims,eps,k", [("exponential", 2000, 12, 0.05, 3), ("uniform", 1500, 6, 0.12, 2)])
+def test_work_counters_equal_oracle(gen, count, dims, eps, k):
+    D = synth.make(gen, count, dims, seed=3) * np.linspace(1.0, 0.5, dims)[::-1]
+    from paper_1809_09930_b200 import Index
+    ix = Index(torch.from_numpy(D).cuda(), eps, k, sample_frac=1.0)
+    st = ix.stats()
+    P, cnt = grid.gpu_join(D, eps, k, reorder=True, sortidu=True, shortc=True, frac=1.0)
+    assert st["cells"] == cnt["cells"]
+    assert st["tests"] == cnt["tests"]
+    assert st["dims"] == cnt["dims"]
+    assert st["pairs"] == len(P)
+
+
+def test_entity_partition_union_equals_single_gpu():
+    D = synth.exponential(4000, 16, seed=21)
+    full, _ = gpu_pairs(D, 0.045, 6)
+    parts = [gpu_pairs(D, 0.045, 6, world=4, rank=r)[0] for r in range(4)]
+    F = {tuple(r) for r in full.tolist()}
+    U = [{tuple(r) for r in p.tolist()} for p in parts]
+    assert sum(len(u) for u in U) == len(F)
+    assert set().union(*U) == F
+
+
+def test_batches_and_host_pipeline_equal_single_launch():
+    from paper_1809_09930_b200 import Index
+    D = synth.exponential(5000, 16, seed=4)
+    ix = Index(torch.from_numpy(D).cuda(), 0.045, 6)
+    cap = ix.estimate(1.0) + 4096
+    out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+    n = ix.self_join(out)
+    ref = {tuple(r) for r in out[:n].cpu().numpy().tolist()}
+    # 5 batches into one device buffer
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for b in range(5):
+        ix.self_join_async(out, cnt, b, 5)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == n
+    assert {tuple(r) for r in out[:n].cpu().numpy().tolist()} == ref
+    # Fig. 4 pipeline into pageable and pinned host buffers, small b_s -> many batches
+    for pinned in (False, True):
+        host = torch.empty((cap, 2), dtype=torch.int32, pin_memory=pinned)
+        m, nb = ix.self_join_host(host, batch_size=max(1, n // 7))
+        assert m == n and nb >= 7
+        assert {tuple(r) for r in host[:m].numpy().tolist()} == ref
+    # capacity error reports the needed size
+    from paper_1809_09930_b200 import GpuJoinError
+    with pytest.raises(GpuJoinError):
+        ix.self_join(out[:10])
+
+
+def test_neighbor_table():
+    from paper_1809_09930_b200 import Index
+    D = synth.exponential(3000, 8, seed=6)
+    ix = Index(torch.from_numpy(D).cuda(), 0.03, 4)
+    out = torch.empty((ix.estimate(1.0) + 4096, 2), dtype=torch.int32, device="cuda")
+    n = ix.self_join(out)
+    off = torch.empty(len(D) + 1, dtype=torch.int64, device="cuda")
+    ix.neighbor_table(out, n, off)
+    p = out[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+    o = off.cpu().numpy()
+    assert o[0] == 0 and o[-1] == n and np.all(np.diff(o) >= 1)       # every point has itself
+    assert np.all(np.diff(p[:, 0] * (1 << 32) + p[:, 1]) > 0)         # strictly sorted
+    for q in (0, 17, 2999):
+        assert np.all(p[o[q]:o[q + 1], 0] == q)
+    sure, amb = brute.self_join(D, 0.03)
+    assert len(amb) == 0 and np.array_equal(sure, p)
+
+
+def test_estimator_is_exact_at_f1_and_close_at_f001():
+    from paper_1809_09930_b200 import Index
+    D = synth.exponential(20000, 16, seed=9)
+    ix = Index(torch.from_numpy(D).cuda(), 0.04, 6)
+    out = torch.empty((ix.estimate(1.0) + 4096, 2), dtype=torch.int32, device="cuda")
+    n = ix.self_join(out)
+    assert ix.estimate(1.0) == n
+    e = ix.estimate(0.01)
+    assert n / 3 <= e <= n * 3
