@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--no-reorder", action="store_true")
     p.add_argument("--no-sortidu", action="store_true")
     p.add_argument("--no-shortc", action="store_true")
+    p.add_argument("--no-symmetric", action="store_true")
     p.add_argument("--batch-size", type=int, default=100_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -179,7 +180,8 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     w = workload(args)
-    flags = dict(reorder=not args.no_reorder, sortidu=not args.no_sortidu, shortc=not args.no_shortc)
+    flags = dict(reorder=not args.no_reorder, sortidu=not args.no_sortidu, shortc=not args.no_shortc,
+                 symmetric=not args.no_symmetric)
 
     # ---- data: generated on rank 0's host; other ranks receive it over NCCL
     N, n = w["count"], w["dims"]
@@ -310,7 +312,7 @@ def main():
     fp64_peak_max = FP64_LANES_PER_SM * 2 * N_SMS * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     roof = None
     if stats is not None:
-        alg_flops = 3.0 * stats["dims"]            # PAPER.md §4.4: 3 flops per dimension term
+        alg_flops = 3.0 * stats["dims_evaluated"]  # PAPER.md §4.4: 3 flops per dimension term
         achieved = alg_flops / (jms / 1000.0) / 1e12 * (world if world > 1 else 1)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
@@ -322,13 +324,14 @@ def main():
                 "frac": achieved / fp64_peak_max, "traffic": traffic,
                 "kernel": "k_join (SelfJoinKernel)",
                 "peak_note": f"derived FP64: {FP64_LANES_PER_SM} FMA lanes x 2 flop x {N_SMS} SMs x max clock",
-                "alg": {"tests": stats["tests"], "dims": stats["dims"], "cells": stats["cells"],
+                "alg": {"tests_evaluated": stats["tests_evaluated"], "dims_evaluated": stats["dims_evaluated"],
+                        "paper_tests": stats["tests"], "paper_dims": stats["dims"], "cells": stats["cells"],
                         "flops_per_dim": 3},
                 "join_ms": jms, "join_share_of_step": jms / ms,
                 "hbm_frac_of_measured": None}
         if peaks.get("hbm_gbs"):
             # bytes the join must at least move: every candidate row read once per tile + pairs written
-            roof["candidate_gbs"] = stats["tests"] * 8.0 * n / 128.0 / (jms / 1000.0) / 1e9
+            roof["candidate_gbs"] = stats["tests_evaluated"] * 8.0 * n / 128.0 / (jms / 1000.0) / 1e9
     line = {
         "metric": "self-join result pairs/s", "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -50,12 +50,14 @@ extern "C" {
 
 typedef struct gj_index gj_index; /* opaque handle */
 
-/* Options of Algorithm 1.  Zero-initialise then set fields; gj_default_options fills them. */
+/* Options of Algorithm 1.  Zero-initialise then set fields; gj_default_options fills them
+ * (reorder = sortidu = shortc = symmetric = 1, sample_frac = 0.01, stream = 0). */
 typedef struct {
     int32_t reorder;     /* 1: REORDER dims by variance (§4.2); 0: index the first k dims */
     int32_t sortidu;     /* 1: SORTIDU prune on the un-indexed dim u (§4.3)               */
     int32_t shortc;      /* 1: SHORTC short-circuit of the distance sum (§4.4)            */
-    int32_t reserved0;
+    int32_t symmetric;   /* 1: evaluate each unordered pair once, emit both orders (default);
+                            0: one full neighbour search per query (Alg. 1 verbatim)        */
     double sample_frac;  /* variance sample fraction (§4.2 "1% of |D|"), in (0,1]        */
     uint64_t stream;     /* cudaStream_t the index issues its work on                     */
 } gj_options;
@@ -75,12 +77,16 @@ typedef struct {
     double build_ms;      /* device time of gj_build_index (CUDA events)           */
 } gj_info;
 
-/* Work counters of one join (gj_join_stats). */
+/* Work counters of one join (gj_join_stats).  cells/tests/dims/pairs are the
+ * paper's per-query counts (Alg. 1 run once per query point), identical for
+ * symmetric and per-query evaluation; *_evaluated is what the kernel ran. */
 typedef struct {
-    int64_t cells;        /* (query, adjacent non-empty cell) visits                        */
-    int64_t tests;        /* candidate distance tests after SORTIDU                         */
-    int64_t dims;         /* dims evaluated with a per-dimension SHORTC check (algorithmic) */
-    int64_t pairs;        /* result pairs (ordered, self pairs included)                    */
+    int64_t cells;           /* (query, adjacent non-empty cell) visits                        */
+    int64_t tests;           /* candidate distance tests after SORTIDU                         */
+    int64_t dims;            /* dims evaluated with a per-dimension SHORTC check (algorithmic) */
+    int64_t pairs;           /* result pairs (ordered, self pairs included)                    */
+    int64_t tests_evaluated; /* distance tests the kernel evaluated (symmetric: unordered)     */
+    int64_t dims_evaluated;  /* per-dimension-SHORTC dims of those tests                        */
 } gj_stats;
 
 GJ_API void gj_default_options(gj_options* opt);
@@ -113,6 +119,13 @@ GJ_API int gj_estimate(gj_index* idx, double frac, int32_t rank, int32_t world, 
 
 /* computeNumBatches (§3.2.2 l.199-200): n_b = max(3, ceil(est / batch_size)). */
 GJ_API int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size);
+
+/* Entity partitioning arithmetic (§6.2 l.1013), host only: the tile positions
+ * j = first + step * m, m in [0, count), of the index's heaviest-first tile
+ * order that rank `rank` of `world` processes in batch `batch` of `n_batches`
+ * (j mod world = rank; (j div world) mod n_batches = batch). */
+GJ_API int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, int32_t n_batches,
+                        int64_t* first, int64_t* step, int64_t* count);
 
 /* selfJoinKernel for one batch (Alg. 1 l.586) [async].
  *  Processes batch `batch` of `n_batches` of rank `rank`'s share of the

@@ -103,6 +103,7 @@ void gj_default_options(gj_options* opt) {
     opt->reorder = 1;
     opt->sortidu = 1;
     opt->shortc = 1;
+    opt->symmetric = 1;
     opt->sample_frac = 0.01;
 }
 
@@ -180,6 +181,21 @@ int gj_device_arrays(const gj_index* h, const double** pts, const uint32_t** ori
     if (!h) { set_error("null argument"); return GJ_ERR_INVALID; }
     if (pts) *pts = h->ix.pts;
     if (orig) *orig = h->ix.orig;
+    return GJ_OK;
+}
+
+int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, int32_t n_batches, int64_t* first,
+                 int64_t* step, int64_t* count) {
+    if (!first || !step || !count || n_tiles < 0) { set_error("bad argument"); return GJ_ERR_INVALID; }
+    if (int rc = check_rank(rank, world)) return rc;
+    if (n_batches < 1 || batch < 0 || batch >= n_batches) { set_error("need 0 <= batch < n_batches"); return GJ_ERR_INVALID; }
+    Index tmp;
+    tmp.T = n_tiles;
+    JoinArgs a{};
+    batch_tiles(&tmp, batch, n_batches, rank, world, &a);
+    *first = a.first;
+    *step = a.step;
+    *count = a.n_tiles;
     return GJ_OK;
 }
 
@@ -382,13 +398,15 @@ int gj_join_stats(gj_index* h, int32_t rank, int32_t world, gj_stats* st) {
     batch_tiles(&ix, 0, 1, rank, world, &a);
     GJ_CUDA(cudaMemsetAsync(ix.scratch_count, 0, 8 * sizeof(uint64_t), ix.stream));
     if (int rc = launch_join(&ix, kStats, a, ix.stream)) return rc;
-    uint64_t c[4];
+    uint64_t c[6];
     GJ_CUDA(cudaMemcpyAsync(c, ix.scratch_count, sizeof(c), cudaMemcpyDeviceToHost, ix.stream));
     GJ_CUDA(cudaStreamSynchronize(ix.stream));
     st->pairs = (int64_t)c[0];
     st->cells = (int64_t)c[1];
     st->tests = (int64_t)c[2];
     st->dims = (int64_t)c[3];
+    st->tests_evaluated = (int64_t)c[4];
+    st->dims_evaluated = (int64_t)c[5];
     return GJ_OK;
 }
 
@@ -422,7 +440,7 @@ void gj_free_index(gj_index* h) {
     if (!h) return;
     Index& ix = h->ix;
     cudaStreamSynchronize(ix.stream);
-    void* ptrs[] = {ix.pts, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.tile_cell, ix.tile_q0,
+    void* ptrs[] = {ix.pts, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
                     ix.tile_order, ix.tile_work, ix.meta, ix.scratch_count};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -193,12 +193,16 @@ __global__ void k_cells(const uint64_t* __restrict__ key, const uint32_t* __rest
 
 // Adjacent non-empty cells (getAdjCells): one warp per cell, lanes split the
 // 3^k offsets (row-major over {-1,0,1}^k), each located by binary search in
-// the sorted id array.  FILL=false: counts + candidate sums; FILL=true: CSR.
+// the sorted id array.  FILL=false: counts + candidate sums (all adjacent
+// cells; and only cells with a larger index, for symmetric evaluation);
+// FILL=true: CSR in offset order (= increasing cell index) + the position of
+// the cell itself in its own list.
 template <bool FILL>
 __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t* __restrict__ cell_start,
                            int64_t G, int k, const Meta* __restrict__ meta, uint32_t* __restrict__ cnt,
-                           uint64_t* __restrict__ cand, const uint32_t* __restrict__ off,
-                           uint32_t* __restrict__ nbr) {
+                           uint64_t* __restrict__ cand, uint64_t* __restrict__ cand_after,
+                           const uint32_t* __restrict__ off, uint32_t* __restrict__ nbr,
+                           uint32_t* __restrict__ nbr_self) {
     __shared__ int64_t s_w[kMaxK];
     __shared__ uint64_t s_s[kMaxK];
     if (threadIdx.x < k) {
@@ -216,7 +220,7 @@ __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t*
     for (int d = 0; d < k; ++d) total *= 3;
     const uint64_t lo_id = cell_id[0], hi_id = cell_id[G - 1];
     uint32_t found = 0, wpos = FILL ? off[g] : 0;
-    uint64_t csum = 0;
+    uint64_t csum = 0, casum = 0;
     for (int64_t o0 = 0; o0 < total; o0 += 32) {
         int64_t o = o0 + lane;
         bool ok = o < total;
@@ -241,19 +245,31 @@ __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t*
         }
         unsigned m = __ballot_sync(0xffffffffu, hit >= 0);
         if (FILL) {
-            if (hit >= 0) nbr[wpos + __popc(m & ((1u << lane) - 1u))] = (uint32_t)hit;
+            if (hit >= 0) {
+                const uint32_t at = wpos + __popc(m & ((1u << lane) - 1u));
+                nbr[at] = (uint32_t)hit;
+                if (hit == g) nbr_self[g] = at;
+            }
             wpos += __popc(m);
         } else {
             found += __popc(m);
-            if (hit >= 0) csum += cell_start[hit + 1] - cell_start[hit];
+            if (hit >= 0) {
+                const uint64_t sz = cell_start[hit + 1] - cell_start[hit];
+                csum += sz;
+                if (hit > g) casum += sz;
+            }
         }
     }
     if (!FILL) {
 #pragma unroll
-        for (int s = 16; s; s >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, s);
+        for (int s = 16; s; s >>= 1) {
+            csum += __shfl_xor_sync(0xffffffffu, csum, s);
+            casum += __shfl_xor_sync(0xffffffffu, casum, s);
+        }
         if (lane == 0) {
             cnt[g] = found;
             cand[g] = csum;
+            cand_after[g] = casum;
         }
     }
 }
@@ -264,7 +280,8 @@ __global__ void k_tile_count(const uint32_t* __restrict__ cell_start, int64_t G,
 }
 
 __global__ void k_tile_fill(const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ toff,
-                            const uint64_t* __restrict__ cand, int64_t G, uint32_t* __restrict__ tile_cell,
+                            const uint64_t* __restrict__ cand, const uint64_t* __restrict__ cand_after, int sym,
+                            int64_t G, uint32_t* __restrict__ tile_cell,
                             uint32_t* __restrict__ tile_q0, uint64_t* __restrict__ tile_work,
                             uint64_t* __restrict__ sort_key, uint32_t* __restrict__ sort_val,
                             unsigned long long* __restrict__ total) {
@@ -274,7 +291,10 @@ __global__ void k_tile_fill(const uint32_t* __restrict__ cell_start, const uint3
     uint32_t t = toff[g];
     for (uint32_t q = a; q < b; q += kTileQ, ++t) {
         uint32_t nq = min((uint32_t)kTileQ, b - q);
-        uint64_t w = (uint64_t)nq * cand[g];
+        // candidate tests of the tile: all adjacent points per query, or (symmetric)
+        // points of later cells plus the later points of the own cell
+        uint64_t w = sym ? (uint64_t)nq * (cand_after[g] + (b - q)) - (uint64_t)nq * (nq + 1) / 2
+                         : (uint64_t)nq * cand[g];
         tile_cell[t] = (uint32_t)g;
         tile_q0[t] = q;
         tile_work[t] = w;
@@ -377,9 +397,11 @@ int build_index(Index* ix, const double* X) {
     // 7. adjacent non-empty cells
     uint32_t* cnt = head;               // reuse (G <= N)
     uint64_t* cand = tmp64;             // reuse: tmp64 no longer needed
+    uint64_t* cand_after = cellkey;     // reuse: cell keys no longer needed
     GJ_CUDA(cudaMallocAsync(&ix->nbr_off, (G + 1) * sizeof(uint32_t), s));
+    GJ_CUDA(cudaMallocAsync(&ix->nbr_self, G * sizeof(uint32_t), s));
     k_adjacent<false><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, cnt, cand,
-                                                             nullptr, nullptr); count_launch();
+                                                             cand_after, nullptr, nullptr, nullptr); count_launch();
     GJ_CUDA(cudaGetLastError());
     if ((rc = scan_u32(cnt, ix->nbr_off, G, d_tot, s))) return rc;
     GJ_CUDA(cudaMemcpyAsync(ix->nbr_off + G, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
@@ -388,7 +410,7 @@ int build_index(Index* ix, const double* X) {
     ix->A = h_tot;
     GJ_CUDA(cudaMallocAsync(&ix->nbr, std::max<int64_t>(1, ix->A) * sizeof(uint32_t), s));
     k_adjacent<true><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, nullptr,
-                                                            nullptr, ix->nbr_off, ix->nbr); count_launch();
+                                                            nullptr, nullptr, ix->nbr_off, ix->nbr, ix->nbr_self); count_launch();
     GJ_CUDA(cudaGetLastError());
     // 8. tiles, heaviest first
     k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, pos); count_launch();
@@ -405,7 +427,8 @@ int build_index(Index* ix, const double* X) {
     unsigned long long* d_total = nullptr;
     GJ_CUDA(cudaMallocAsync(&d_total, sizeof(*d_total), s));
     GJ_CUDA(cudaMemsetAsync(d_total, 0, sizeof(*d_total), s));
-    k_tile_fill<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, pos, cand, G, ix->tile_cell, ix->tile_q0,
+    k_tile_fill<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, pos, cand, cand_after, ix->opt.symmetric, G,
+                                                   ix->tile_cell, ix->tile_q0,
                                                    ix->tile_work, skey, ix->tile_order, d_total); count_launch();
     GJ_CUDA(cudaGetLastError());
     if ((rc = varying_bits_u64(skey, T, &vb, s))) return rc;

@@ -55,6 +55,7 @@ struct Index {
     uint32_t* cell_start = nullptr;  // [G+1]
     uint32_t* nbr_off = nullptr;     // [G+1]
     uint32_t* nbr = nullptr;         // [A] adjacent non-empty cells (offset order)
+    uint32_t* nbr_self = nullptr;    // [G] position of cell g inside its own adjacency list
     uint32_t* tile_cell = nullptr;   // [T]
     uint32_t* tile_q0 = nullptr;     // [T]
     uint32_t* tile_order = nullptr;  // [T] tiles, heaviest estimated work first

@@ -1,5 +1,11 @@
 // SelfJoinKernel (Alg. 1 l.596-607) for sm_100a.
 //
+// Symmetric mode (default): dist(a,b) = dist(b,a) bit-for-bit (the per-dim
+// squares are identical), so each unordered pair is evaluated once -- a tile
+// of cell A visits only adjacent cells with index >= A, and in A itself only
+// candidates after the query -- and both ordered pairs are emitted; the self
+// pair is emitted directly.  Per-query mode (symmetric = 0) is Alg. 1 verbatim.
+//
 // One CTA = one query tile: up to 128 consecutive sorted points of ONE
 // non-empty cell A (so the whole CTA shares getAdjCells' result, computed
 // once per cell at index build).  One thread = one query point, its n
@@ -28,6 +34,7 @@ struct Params {
     const uint32_t* __restrict__ cell_start;
     const uint32_t* __restrict__ nbr_off;
     const uint32_t* __restrict__ nbr;
+    const uint32_t* __restrict__ nbr_self;
     const uint32_t* __restrict__ tile_cell;
     const uint32_t* __restrict__ tile_q0;
     const uint32_t* __restrict__ tile_order;
@@ -37,15 +44,36 @@ struct Params {
 
 constexpr int kSmemDoubles = 4096;   // 32 KB candidate stage
 
-template <int NPR, int MODE>
+// Stats mode: one candidate with the oracle's exact arithmetic (unfused,
+// dimension order, SHORTC check after every dimension).  Returns dims used.
+template <int NPR>
+__device__ __forceinline__ int dims_exact(const double (&q)[NPR], const double* __restrict__ cp, int n,
+                                          double eps2, double* acc_out) {
+    double acc = 0.0;
+    int used = 0;
+#pragma unroll
+    for (int d = 0; d < NPR; ++d) {
+        if (d >= n) break;
+        const double t = __dsub_rn(q[d], cp[d]);
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+        ++used;
+        if (acc > eps2) break;
+    }
+    *acc_out = acc;
+    return used;
+}
+
+// Counters (kCount/kStats): 0 pairs, 1 cells, 2 tests, 3 dims, 4 tests evaluated, 5 dims evaluated.
+template <int NPR, int MODE, bool SYM>
 __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
-    constexpr int TC = kSmemDoubles / NPR;
+    constexpr int TC = kSmemDoubles / NPR;   // candidates per shared-memory stage (even)
     __shared__ __align__(16) double Cs[kSmemDoubles];
     __shared__ uint32_t Cid[TC];
     __shared__ uint32_t s_win[2];
-    __shared__ unsigned long long s_red[4][kTileQ / 32];
+    __shared__ unsigned long long s_red[6][kTileQ / 32];
 
     const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const int64_t j = A.first + A.step * (int64_t)blockIdx.x;
     const uint32_t tile = P.tile_order[j];
     const uint32_t g = P.tile_cell[tile];
@@ -68,15 +96,34 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     const uint32_t qid = P.orig[qpos];
     const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
+    constexpr unsigned long long kMul = SYM ? 2ull : 1ull;   // ordered pairs per evaluated pair
 
-    uint64_t c_cells = 0, c_tests = 0, c_dims = 0, c_pairs = 0;
-    const uint32_t nb0 = P.nbr_off[g], nb1 = P.nbr_off[g + 1];
+    unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
+    if (MODE == kStats && active) cnt[1] += P.nbr_off[g + 1] - P.nbr_off[g];
+    if (SYM) {   // the self pair (q, q): d = 0 <= eps
+        if (MODE == kEmit) {
+            const unsigned m = __ballot_sync(0xffffffffu, active);
+            unsigned long long base = 0;
+            if (lane == 0 && m) base = atomicAdd((unsigned long long*)A.count, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (active) {
+                const unsigned long long at = base + __popc(m & lt);
+                if (at < A.cap) reinterpret_cast<uint2*>(A.out)[at] = make_uint2(qid, qid);
+            }
+        } else if (active) {
+            cnt[0] += 1;
+            cnt[2] += 1;
+            cnt[3] += P.n;
+        }
+    }
+
+    const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
     for (uint32_t b = nb0; b < nb1; ++b) {
         const uint32_t B = P.nbr[b];
         uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
-        if (P.sortidu) {
+        if (P.sortidu) {   // tile-level SORTIDU window: union of the queries' u-windows
             __syncthreads();
-            if (tid < 2) {   // lane 0: first r with u_lo - r(u) <= eps; lane 1: first s with s(u) - u_hi > eps
+            if (tid < 2) {   // tid 0: first r with u_lo - r(u) <= eps; tid 1: first s with s(u) - u_hi > eps
                 uint32_t lo = r, hi = s;
                 while (lo < hi) {
                     uint32_t mid = (lo + hi) >> 1;
@@ -90,79 +137,113 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
             r = s_win[0];
             s = max(s_win[1], r);
         }
-        if (MODE == kStats && active) ++c_cells;
+        const bool diag = SYM && B == g;
+        if (diag) r = max(r, q0 + 1);   // own cell: only candidates after the query
         for (uint32_t cb = r; cb < s; cb += TC) {
-            const int cnt = (int)min((uint32_t)TC, s - cb);
+            const int cntc = (int)min((uint32_t)TC, s - cb);
             __syncthreads();
             {
                 const double2* src = reinterpret_cast<const double2*>(P.pts + (size_t)cb * n_pad);
                 double2* dst = reinterpret_cast<double2*>(Cs);
-                const int nv = cnt * n_pad / 2;
+                const int nv = cntc * n_pad / 2;
                 for (int i = tid; i < nv; i += kTileQ) dst[i] = src[i];
-                for (int i = tid; i < cnt; i += kTileQ) Cid[i] = P.orig[cb + i];
+                for (int i = tid; i < cntc; i += kTileQ) Cid[i] = P.orig[cb + i];
             }
             __syncthreads();
-            for (int c = 0; c < cnt; ++c) {
-                const double* cp = Cs + c * n_pad;
-                bool ok = active;
-                if (P.sortidu) {
-                    const double cu = cp[P.u];
-                    ok = ok && (qu - cu <= eps) && (cu - qu <= eps);
+            for (int c = 0; c < cntc; c += 2) {
+                const bool two = c + 1 < cntc;
+                const double* cp0 = Cs + c * n_pad;
+                const double* cp1 = two ? cp0 + n_pad : cp0;
+                const uint32_t p0 = cb + c;
+                bool ok0 = active, ok1 = active && two;
+                if (diag) {
+                    ok0 = ok0 && p0 > qpos;
+                    ok1 = ok1 && p0 + 1 > qpos;
                 }
-                double acc = 0.0;
-                if (ok) {
-                    if (MODE == kStats) {
-                        ++c_tests;
-                        int used = 0;
-#pragma unroll
-                        for (int d = 0; d < NPR; ++d) {
-                            if (d >= P.n) break;
-                            // unfused, in dimension order: the oracle's arithmetic
-                            const double t = __dsub_rn(q[d], cp[d]);
-                            acc = __dadd_rn(acc, __dmul_rn(t, t));
-                            ++used;
-                            if (acc > eps2) break;
-                        }
-                        c_dims += used;
-                    } else {
+                double a0, a1;
+                if (MODE == kStats) {
+                    if (P.sortidu) {   // the paper's per-query window |p(u) - q(u)| <= eps
+                        const double c0u = cp0[P.u], c1u = cp1[P.u];
+                        ok0 = ok0 && (qu - c0u <= eps) && (c0u - qu <= eps);
+                        ok1 = ok1 && (qu - c1u <= eps) && (c1u - qu <= eps);
+                    }
+                    a0 = a1 = INFINITY;
+                    if (ok0) {
+                        const unsigned long long used = dims_exact<NPR>(q, cp0, P.n, eps2, &a0);
+                        cnt[2] += kMul; cnt[3] += kMul * used; cnt[4] += 1; cnt[5] += used;
+                    }
+                    if (ok1) {
+                        const unsigned long long used = dims_exact<NPR>(q, cp1, P.n, eps2, &a1);
+                        cnt[2] += kMul; cnt[3] += kMul * used; cnt[4] += 1; cnt[5] += used;
+                    }
+                } else {
+                    // two independent candidates per thread (two FMA chains in flight);
+                    // a dead candidate starts at +inf so it never keeps the loop alive
+                    a0 = ok0 ? 0.0 : INFINITY;
+                    a1 = ok1 ? 0.0 : INFINITY;
+                    if (ok0 || ok1) {
 #pragma unroll
                         for (int d = 0; d < NPR; d += 4) {
                             if (d >= n_pad) break;
-                            const double2 a = *reinterpret_cast<const double2*>(cp + d);
-                            const double2 b2 = *reinterpret_cast<const double2*>(cp + d + 2);
-                            double t0 = q[d] - a.x, t1 = q[d + 1] - a.y, t2 = q[d + 2] - b2.x, t3 = q[d + 3] - b2.y;
-                            acc = fma(t0, t0, acc);
-                            acc = fma(t1, t1, acc);
-                            acc = fma(t2, t2, acc);
-                            acc = fma(t3, t3, acc);
-                            if (P.shortc && acc > eps2) break;
+                            const double2 x0 = *reinterpret_cast<const double2*>(cp0 + d);
+                            const double2 y0 = *reinterpret_cast<const double2*>(cp0 + d + 2);
+                            const double2 x1 = *reinterpret_cast<const double2*>(cp1 + d);
+                            const double2 y1 = *reinterpret_cast<const double2*>(cp1 + d + 2);
+                            double t;
+                            t = q[d] - x0.x;     a0 = fma(t, t, a0);
+                            t = q[d] - x1.x;     a1 = fma(t, t, a1);
+                            t = q[d + 1] - x0.y; a0 = fma(t, t, a0);
+                            t = q[d + 1] - x1.y; a1 = fma(t, t, a1);
+                            t = q[d + 2] - y0.x; a0 = fma(t, t, a0);
+                            t = q[d + 2] - y1.x; a1 = fma(t, t, a1);
+                            t = q[d + 3] - y0.y; a0 = fma(t, t, a0);
+                            t = q[d + 3] - y1.y; a1 = fma(t, t, a1);
+                            if (P.shortc && a0 > eps2 && a1 > eps2) break;   // SHORTC
                         }
                     }
                 }
-                const bool hit = ok && acc <= eps2;
+                const bool hit0 = ok0 && a0 <= eps2, hit1 = ok1 && a1 <= eps2;
                 if (MODE == kEmit) {
-                    const unsigned m = __ballot_sync(0xffffffffu, hit);
-                    if (m) {
-                        const int leader = __ffs(m) - 1;
+                    const unsigned m0 = __ballot_sync(0xffffffffu, hit0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, hit1);
+                    if (m0 | m1) {
+                        const int leader = __ffs(m0 | m1) - 1;
                         unsigned long long base = 0;
-                        if (lane == leader) base = atomicAdd((unsigned long long*)A.count, (unsigned long long)__popc(m));
+                        if (lane == leader)
+                            base = atomicAdd((unsigned long long*)A.count, kMul * (__popc(m0) + __popc(m1)));
                         base = __shfl_sync(0xffffffffu, base, leader);
-                        if (hit) {
-                            const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
-                            if (at < A.cap) reinterpret_cast<uint2*>(A.out)[at] = make_uint2(qid, Cid[c]);
+                        uint2* out = reinterpret_cast<uint2*>(A.out);
+                        if (hit0) {
+                            const unsigned long long at = base + kMul * __popc(m0 & lt);
+                            const uint32_t id = Cid[c];
+                            if (at + kMul <= A.cap) {
+                                out[at] = make_uint2(qid, id);
+                                if (SYM) out[at + 1] = make_uint2(id, qid);
+                            }
+                        }
+                        if (hit1) {
+                            const unsigned long long at = base + kMul * (__popc(m0) + __popc(m1 & lt));
+                            const uint32_t id = Cid[c + 1];
+                            if (at + kMul <= A.cap) {
+                                out[at] = make_uint2(qid, id);
+                                if (SYM) out[at + 1] = make_uint2(id, qid);
+                            }
                         }
                     }
                 } else {
-                    c_pairs += hit;
+                    cnt[0] += kMul * ((unsigned long long)hit0 + (unsigned long long)hit1);
                 }
             }
         }
     }
     if (MODE != kEmit) {
-        unsigned long long v[4] = {c_pairs, c_cells, c_tests, c_dims};
-        const int nv = MODE == kStats ? 4 : 1;
+        if (MODE == kStats && !SYM) {
+            cnt[4] = cnt[2];
+            cnt[5] = cnt[3];
+        }
+        const int nv = MODE == kStats ? 6 : 1;
         for (int i = 0; i < nv; ++i) {
-            unsigned long long x = v[i];
+            unsigned long long x = cnt[i];
 #pragma unroll
             for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
             if (lane == 0) s_red[i][tid >> 5] = x;
@@ -177,13 +258,19 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     }
 }
 
-template <int NPR>
-int launch_np(const Params& p, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
-    if (a.n_tiles <= 0) return GJ_OK;
+template <int NPR, bool SYM>
+void launch_mode(const Params& p, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     dim3 grid((unsigned)a.n_tiles);
-    if (mode == kEmit) k_join<NPR, kEmit><<<grid, kTileQ, 0, s>>>(p, a);
-    else if (mode == kCount) k_join<NPR, kCount><<<grid, kTileQ, 0, s>>>(p, a);
-    else k_join<NPR, kStats><<<grid, kTileQ, 0, s>>>(p, a);
+    if (mode == kEmit) k_join<NPR, kEmit, SYM><<<grid, kTileQ, 0, s>>>(p, a);
+    else if (mode == kCount) k_join<NPR, kCount, SYM><<<grid, kTileQ, 0, s>>>(p, a);
+    else k_join<NPR, kStats, SYM><<<grid, kTileQ, 0, s>>>(p, a);
+}
+
+template <int NPR>
+int launch_np(const Params& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
+    if (a.n_tiles <= 0) return GJ_OK;
+    if (sym) launch_mode<NPR, true>(p, mode, a, s);
+    else launch_mode<NPR, false>(p, mode, a, s);
     count_launch();
     GJ_CUDA(cudaGetLastError());
     return GJ_OK;
@@ -205,6 +292,7 @@ int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t 
     p.cell_start = ix->cell_start;
     p.nbr_off = ix->nbr_off;
     p.nbr = ix->nbr;
+    p.nbr_self = ix->nbr_self;
     p.tile_cell = ix->tile_cell;
     p.tile_q0 = ix->tile_q0;
     p.tile_order = ix->tile_order;
@@ -216,14 +304,15 @@ int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t 
     p.eps = ix->eps;
     p.eps2 = ix->eps2;
     const int np = ix->n_pad;
-    if (np <= 8) return launch_np<8>(p, mode, a, s);
-    if (np <= 16) return launch_np<16>(p, mode, a, s);
-    if (np <= 24) return launch_np<24>(p, mode, a, s);
-    if (np <= 32) return launch_np<32>(p, mode, a, s);
-    if (np <= 48) return launch_np<48>(p, mode, a, s);
-    if (np <= 64) return launch_np<64>(p, mode, a, s);
-    if (np <= 96) return launch_np<96>(p, mode, a, s);
-    return launch_np<128>(p, mode, a, s);
+    const bool sym = ix->opt.symmetric != 0;
+    if (np <= 8) return launch_np<8>(p, mode, a, sym, s);
+    if (np <= 16) return launch_np<16>(p, mode, a, sym, s);
+    if (np <= 24) return launch_np<24>(p, mode, a, sym, s);
+    if (np <= 32) return launch_np<32>(p, mode, a, sym, s);
+    if (np <= 48) return launch_np<48>(p, mode, a, sym, s);
+    if (np <= 64) return launch_np<64>(p, mode, a, sym, s);
+    if (np <= 96) return launch_np<96>(p, mode, a, sym, s);
+    return launch_np<128>(p, mode, a, sym, s);
 }
 
 }  // namespace gj

@@ -19,13 +19,13 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 
 # Every symbol include/gpujoin.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
-           "gj_estimate", "gj_num_batches", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
+           "gj_estimate", "gj_num_batches", "gj_partition", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
            "gj_self_join_host", "gj_join_stats", "gj_neighbor_table", "gj_free_index", "gj_last_error",
            "gj_abi_version", "gj_launch_count"]
 
 
 class Options(C.Structure):
-    _fields_ = [("reorder", C.c_int32), ("sortidu", C.c_int32), ("shortc", C.c_int32), ("reserved0", C.c_int32),
+    _fields_ = [("reorder", C.c_int32), ("sortidu", C.c_int32), ("shortc", C.c_int32), ("symmetric", C.c_int32),
                 ("sample_frac", C.c_double), ("stream", C.c_uint64)]
 
 
@@ -36,7 +36,8 @@ class Info(C.Structure):
 
 
 class Stats(C.Structure):
-    _fields_ = [("cells", C.c_int64), ("tests", C.c_int64), ("dims", C.c_int64), ("pairs", C.c_int64)]
+    _fields_ = [("cells", C.c_int64), ("tests", C.c_int64), ("dims", C.c_int64), ("pairs", C.c_int64),
+                ("tests_evaluated", C.c_int64), ("dims_evaluated", C.c_int64)]
 
 
 class GpuJoinError(RuntimeError):
@@ -65,6 +66,7 @@ def lib():
         "gj_device_arrays": (C.c_int, [P, C.POINTER(P), C.POINTER(P)]),
         "gj_estimate": (C.c_int, [P, D, I32, I32, C.POINTER(I64)]),
         "gj_num_batches": (I64, [I64, I64]),
+        "gj_partition": (C.c_int, [I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
         "gj_self_join_async": (C.c_int, [P, P, I64, P, I32, I32, I32, I32]),
         "gj_self_join_count_async": (C.c_int, [P, P, I32, I32, I32, I32]),
         "gj_self_join": (C.c_int, [P, P, I64, I32, I32, C.POINTER(I64)]),
@@ -89,10 +91,10 @@ def _check(rc):
         raise GpuJoinError(rc, lib().gj_last_error().decode())
 
 
-def default_options(reorder=True, sortidu=True, shortc=True, sample_frac=0.01, stream=0) -> Options:
+def default_options(reorder=True, sortidu=True, shortc=True, sample_frac=0.01, stream=0, symmetric=True) -> Options:
     o = Options()
     lib().gj_default_options(C.byref(o))
-    o.reorder, o.sortidu, o.shortc = int(reorder), int(sortidu), int(shortc)
+    o.reorder, o.sortidu, o.shortc, o.symmetric = int(reorder), int(sortidu), int(shortc), int(symmetric)
     o.sample_frac = float(sample_frac)
     o.stream = int(stream)
     return o
@@ -111,7 +113,7 @@ class _CudaView:
     """__cuda_array_interface__ wrapper of a raw device pointer (read-only view)."""
 
     def __init__(self, ptr, shape, typestr):
-        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=typestr, data=(int(ptr), True),
+        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=typestr, data=(int(ptr), False),
                                              version=3, strides=None)
 
 
@@ -120,7 +122,7 @@ class Index:
     tensor (stays on the device) or a host numpy array / tensor (staged)."""
 
     def __init__(self, points, eps: float, k: int, reorder=True, sortidu=True, shortc=True, sample_frac=0.01,
-                 stream=None):
+                 stream=None, symmetric=True):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
@@ -132,7 +134,7 @@ class Index:
         self._keep = points
         n, dim = points.shape
         self.n_points, self.dim = int(n), int(dim)
-        self.options = default_options(reorder, sortidu, shortc, sample_frac, stream)
+        self.options = default_options(reorder, sortidu, shortc, sample_frac, stream, symmetric)
         h = C.c_void_p()
         _check(lib().gj_build_index(_ptr(points), n, dim, float(eps), int(k), C.byref(self.options), C.byref(h)))
         self._h = h
@@ -200,7 +202,8 @@ class Index:
     def stats(self, rank=0, world=1) -> dict:
         s = Stats()
         _check(lib().gj_join_stats(self._h, rank, world, C.byref(s)))
-        return dict(cells=s.cells, tests=s.tests, dims=s.dims, pairs=s.pairs)
+        return dict(cells=s.cells, tests=s.tests, dims=s.dims, pairs=s.pairs, tests_evaluated=s.tests_evaluated,
+                    dims_evaluated=s.dims_evaluated)
 
     def neighbor_table(self, pairs, n_pairs, offsets):
         _check(lib().gj_neighbor_table(self._h, _ptr(pairs), int(n_pairs), _ptr(offsets)))
@@ -219,6 +222,13 @@ class Index:
 
 def num_batches(est_pairs: int, batch_size: int) -> int:
     return int(lib().gj_num_batches(int(est_pairs), int(batch_size)))
+
+
+def partition(n_tiles: int, rank: int, world: int, batch: int = 0, n_batches: int = 1):
+    """(first, step, count) of the tile positions of (rank, batch) -- gj_partition."""
+    f, s, c = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().gj_partition(int(n_tiles), rank, world, batch, n_batches, C.byref(f), C.byref(s), C.byref(c)))
+    return f.value, s.value, c.value
 
 
 def launch_count() -> int:

@@ -53,7 +53,7 @@ SMALL = [  # (generator, |D|, n, eps, k)
     ("exponential", 2500, 32, 0.08, 6),
     ("exponential", 1500, 64, 0.16, 6),
     ("uniform", 3000, 3, 0.02, 2),
-    ("uniform", 1000, 90, 1.2, 8),
+    ("uniform", 1000, 90, 3.1, 8),
     ("exponential", 1777, 18, 0.05, 1),   # ragged tiles, k = 1
     ("exponential", 900, 5, 0.05, 5),     # k = n (u = dim 1)
 ]
@@ -67,10 +67,11 @@ def test_pairs_equal_brute_force(gen, count, dims, eps, k):
     assert len(got) > count                       # real neighbours, not just self pairs
 
 
-@pytest.mark.parametrize("reorder,sortidu,shortc", [(r, s, c) for r in (0, 1) for s in (0, 1) for c in (0, 1)])
-def test_every_flag_combination(reorder, sortidu, shortc):
+@pytest.mark.parametrize("reorder,sortidu,shortc,symmetric",
+                         [(r, s, c, y) for r in (0, 1) for s in (0, 1) for c in (0, 1) for y in (0, 1)])
+def test_every_flag_combination(reorder, sortidu, shortc, symmetric):
     D = synth.exponential(2200, 24, seed=5)
-    got, _ = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc)
+    got, _ = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc, symmetric=symmetric)
     check(D, 0.07, got)
 
 
@@ -118,23 +119,30 @@ def test_index_structure_matches_algorithm1_oracle():
     assert np.array_equal(pts[:, :D.shape[1]].cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("symmetric", [0, 1])
 @pytest.mark.parametrize("gen,count,dims,eps,k", [("exponential", 2000, 12, 0.05, 3), ("uniform", 1500, 6, 0.12, 2)])
-def test_work_counters_equal_oracle(gen, count, dims, eps, k):
+def test_work_counters_equal_oracle(gen, count, dims, eps, k, symmetric):
     D = synth.make(gen, count, dims, seed=3) * np.linspace(1.0, 0.5, dims)[::-1]
     from paper_1809_09930_b200 import Index
-    ix = Index(torch.from_numpy(D).cuda(), eps, k, sample_frac=1.0)
+    ix = Index(torch.from_numpy(D).cuda(), eps, k, sample_frac=1.0, symmetric=symmetric)
     st = ix.stats()
     P, cnt = grid.gpu_join(D, eps, k, reorder=True, sortidu=True, shortc=True, frac=1.0)
     assert st["cells"] == cnt["cells"]
     assert st["tests"] == cnt["tests"]
     assert st["dims"] == cnt["dims"]
     assert st["pairs"] == len(P)
+    if symmetric:   # each unordered pair once; the self test is not evaluated
+        assert 2 * st["tests_evaluated"] + count == cnt["tests"]
+        assert 2 * st["dims_evaluated"] + count * dims == cnt["dims"]
+    else:
+        assert st["tests_evaluated"] == cnt["tests"] and st["dims_evaluated"] == cnt["dims"]
 
 
-def test_entity_partition_union_equals_single_gpu():
+@pytest.mark.parametrize("symmetric", [0, 1])
+def test_entity_partition_union_equals_single_gpu(symmetric):
     D = synth.exponential(4000, 16, seed=21)
-    full, _ = gpu_pairs(D, 0.045, 6)
-    parts = [gpu_pairs(D, 0.045, 6, world=4, rank=r)[0] for r in range(4)]
+    full, _ = gpu_pairs(D, 0.045, 6, symmetric=symmetric)
+    parts = [gpu_pairs(D, 0.045, 6, world=4, rank=r, symmetric=symmetric)[0] for r in range(4)]
     F = {tuple(r) for r in full.tolist()}
     U = [{tuple(r) for r in p.tolist()} for p in parts]
     assert sum(len(u) for u in U) == len(F)
