@@ -98,3 +98,21 @@ def test_neighbors_of_matches_rows():
     for qi, (s, a) in zip(q, brute.neighbors_of(D, 0.04, q, chunk=128)):
         assert list(s) == list(sure[sure[:, 0] == qi][:, 1])
         assert len(a) == 0
+
+
+def test_selectivity_calibration_golden_supports_reading_r1():
+    """tests/golden/selectivity_calibration.txt (written by its generator
+    script from oracle/ + synth/ only): under reading R1 the exponential sets
+    reproduce the paper's S_D ranges (Fig. 5 caption, l.969), min/max
+    renormalised ones give S_D ~ 0.  Re-derives the 16-d eps=0.03 row."""
+    import os
+    rows = np.loadtxt(os.path.join(os.path.dirname(__file__), "golden", "selectivity_calibration.txt"), ndmin=2)
+    paper = {(16, 0.03): 4, (16, 0.05): 1200, (32, 0.08): 31, (32, 0.10): 1400, (64, 0.16): 132, (64, 0.18): 2300}
+    for dims, eps, raw, nrm in rows:
+        ref = paper[(int(dims), round(eps, 2))]
+        assert ref / 2.5 <= raw <= ref * 2.5, (dims, eps, raw, ref)
+        assert nrm < 0.1
+    D = synth.exponential(2_000_000, 16, seed=0)
+    q = synth.query_sample(len(D), 100, seed=1)
+    sd = np.mean([len(s) + len(a) - 1 for s, a in brute.neighbors_of(D, 0.03, q)])
+    assert abs(sd - rows[0, 2]) < 0.01
