@@ -91,7 +91,7 @@ using namespace gj;
 
 extern "C" {
 
-int32_t gj_abi_version(void) { return 1; }
+int32_t gj_abi_version(void) { return 2; }
 
 int64_t gj_launch_count(void) { return (int64_t)g_launches.load(); }
 
@@ -104,6 +104,7 @@ void gj_default_options(gj_options* opt) {
     opt->sortidu = 1;
     opt->shortc = 1;
     opt->symmetric = 1;
+    opt->fp32_filter = 1;
     opt->sample_frac = 0.01;
 }
 
@@ -130,6 +131,7 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     ix.eps2 = eps * eps;
     ix.opt = o;
     ix.stream = (cudaStream_t)o.stream;
+    ix.fp32_filter = o.fp32_filter ? 1 : 0;
     const double* dX = points;
     double* staged = nullptr;
     int rc = GJ_OK;
@@ -168,6 +170,9 @@ int gj_index_info(const gj_index* h, gj_info* info) {
     info->n_tiles = ix.T;
     info->est_candidates = ix.est_candidates;
     info->build_ms = ix.build_ms;
+    info->fp32_filter = ix.fp32_filter;
+    info->filter_threshold = ix.thr32;
+    info->filter_margin = ix.filter_margin;
     return GJ_OK;
 }
 
@@ -440,7 +445,7 @@ void gj_free_index(gj_index* h) {
     if (!h) return;
     Index& ix = h->ix;
     cudaStreamSynchronize(ix.stream);
-    void* ptrs[] = {ix.pts, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
+    void* ptrs[] = {ix.pts, ix.pts32, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
                     ix.tile_order, ix.tile_work, ix.meta, ix.scratch_count};
     for (void* p : ptrs)
         if (p) cudaFree(p);

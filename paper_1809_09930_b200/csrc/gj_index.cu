@@ -19,6 +19,8 @@
 // R7 u = position k if k < n else 0; R9 first indexed dim most significant.
 #include <math.h>
 
+#include <cmath>
+
 #include <algorithm>
 #include <vector>
 
@@ -163,16 +165,25 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* _
 }
 
 // pts[p][t] = X[idx[p]][order[t]] (0 for t >= n); one thread per output element.
+// pts32 (optional): the same coordinate centred on the dimension minimum and
+// rounded to float32, fl32(x - min) -- input of the certified FP32 prefilter.
 __global__ void k_gather_points(const double* __restrict__ X, const uint32_t* __restrict__ idx, int64_t N,
-                                int n, int n_pad, const Meta* __restrict__ meta, double* __restrict__ pts) {
+                                int n, int n_pad, const Meta* __restrict__ meta, double* __restrict__ pts,
+                                float* __restrict__ pts32) {
     __shared__ int ord[kMaxDim];
-    for (int t = threadIdx.x; t < n; t += blockDim.x) ord[t] = meta->order[t];
+    __shared__ double mn[kMaxDim];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        ord[t] = meta->order[t];
+        mn[t] = meta->mins[ord[t]];
+    }
     __syncthreads();
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= N * n_pad) return;
     int64_t p = e / n_pad;
     int t = (int)(e - p * n_pad);
-    pts[e] = t < n ? X[(int64_t)idx[p] * n + ord[t]] : 0.0;
+    const double x = t < n ? X[(int64_t)idx[p] * n + ord[t]] : 0.0;
+    pts[e] = x;
+    if (pts32) pts32[e] = t < n ? __double2float_rn(x - mn[t]) : 0.0f;
 }
 
 __global__ void k_heads(const uint64_t* __restrict__ key, int64_t N, uint32_t* __restrict__ head) {
@@ -321,6 +332,35 @@ int col_reduce(const double* X, int64_t m, int64_t rstride, int n, int mode, con
 
 inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
+// Threshold of the certified FP32 prefilter (DESIGN.md §"FP32 prefilter").
+// With x' = fl32(x - min_j), s_j = max_j - min_j, u = 2^-24:
+//   |fl32(q'_j - c'_j) - (q_j - c_j)| <= a_j = 4.001 u s_j          (per dim)
+//   ||delta~|| >= ||delta|| - A,  A = ||a|| (+ a subnormal slack)
+//   fp32 recursive FMA sum S~_k of k <= n squares: S~_k <= (1 + gamma_n) sum_all delta~^2
+// so S~_k > T = (1 + gamma_n) (eps (1 + 1e-9) + A)^2 proves ||delta|| > eps (1 + 1e-9):
+// the pair is outside eps and outside the 1e-12 ambiguity band.  Every pair the
+// filter does not reject is decided by the FP64 test.  The filter is switched
+// off when it could not reject much (A > 1e-3 eps) or fp32 could overflow.
+void fp32_threshold(Index* ix) {
+    const Meta& m = ix->h_meta;
+    double ss = 0.0, smax = 0.0;
+    for (int t = 0; t < ix->n; ++t) {
+        const int o = m.order[t];
+        const double sj = m.maxs[o] - m.mins[o];
+        ss += sj * sj;
+        smax = std::max(smax, sj);
+    }
+    const double u = std::ldexp(1.0, -24);
+    const double A = 4.001 * u * std::sqrt(ss) * (1.0 + 1e-12) + std::sqrt((double)ix->n) * std::ldexp(1.0, -147);
+    const double gamma = ix->n * u / (1.0 - ix->n * u);
+    const double T = (1.0 + gamma) * (ix->eps * (1.0 + 1e-9) + A) * (ix->eps * (1.0 + 1e-9) + A);
+    float T32 = (float)T;
+    if ((double)T32 < T) T32 = std::nextafter(T32, INFINITY);
+    ix->filter_margin = T / (ix->eps * ix->eps) - 1.0;
+    ix->thr32 = T32;
+    if (!(smax < 1e30) || !(T32 < 1e30f) || A > 1e-3 * ix->eps) ix->fp32_filter = 0;
+}
+
 }  // namespace
 
 int build_index(Index* ix, const double* X) {
@@ -354,6 +394,7 @@ int build_index(Index* ix, const double* X) {
         set_error("linearized cell id needs >= 2^63 cells (prod of per-dim widths); choose a smaller k");
         return GJ_ERR_OVERFLOW;
     }
+    fp32_threshold(ix);
     // 3. keys
     uint64_t *cellkey = nullptr, *ukey = nullptr, *tmp64 = nullptr;
     uint32_t* idx = nullptr;
@@ -376,7 +417,8 @@ int build_index(Index* ix, const double* X) {
     // 5. sorted, reordered point array
     GJ_CUDA(cudaMallocAsync(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
     GJ_CUDA(cudaMallocAsync(&ix->orig, N * sizeof(uint32_t), s));
-    k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts); count_launch();
+    if (ix->fp32_filter) GJ_CUDA(cudaMallocAsync(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
+    k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, ix->pts32); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     // 6. non-empty cells
     uint32_t *head = nullptr, *pos = nullptr, *d_tot = nullptr;

@@ -50,6 +50,10 @@ struct Index {
     cudaStream_t stream = 0;
     // device arrays
     double* pts = nullptr;           // [N][n_pad] reordered dims, sorted by (cell, u)
+    float* pts32 = nullptr;          // [N][n_pad] fl32(x - min_j): input of the certified FP32 prefilter
+    int fp32_filter = 0;             // 1: join kernel runs the FP32 prefilter + FP64 decision
+    float thr32 = 0.f;               // prefilter rejection threshold (> eps^2, see fp32_threshold)
+    double filter_margin = 0;        // thr32 / eps^2 - 1
     uint32_t* orig = nullptr;        // [N] sorted position -> original id
     uint64_t* cell_id = nullptr;     // [G] sorted non-empty linear ids
     uint32_t* cell_start = nullptr;  // [G+1]
@@ -92,7 +96,25 @@ struct JoinArgs {
     int64_t step;             // tile positions j = first + step * m
     int64_t n_tiles;          // number of m values
 };
+struct JoinParams {
+    const double* __restrict__ pts;
+    const float* __restrict__ pts32;
+    const uint32_t* __restrict__ orig;
+    const uint32_t* __restrict__ cell_start;
+    const uint32_t* __restrict__ nbr_off;
+    const uint32_t* __restrict__ nbr;
+    const uint32_t* __restrict__ nbr_self;
+    const uint32_t* __restrict__ tile_cell;
+    const uint32_t* __restrict__ tile_q0;
+    const uint32_t* __restrict__ tile_order;
+    int n, n_pad, u, sortidu, shortc;
+    double eps, eps2;
+    float thr32;
+};
+JoinParams join_params(const Index* ix);
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+// FP32-prefilter variant (gj_join32.cu); kEmit / kCount only.
+int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // Number of tile positions for (rank, world, batch, n_batches); sets first/step.
 void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
                  JoinArgs* a);

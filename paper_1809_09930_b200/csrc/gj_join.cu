@@ -28,19 +28,7 @@
 namespace gj {
 namespace {
 
-struct Params {
-    const double* __restrict__ pts;
-    const uint32_t* __restrict__ orig;
-    const uint32_t* __restrict__ cell_start;
-    const uint32_t* __restrict__ nbr_off;
-    const uint32_t* __restrict__ nbr;
-    const uint32_t* __restrict__ nbr_self;
-    const uint32_t* __restrict__ tile_cell;
-    const uint32_t* __restrict__ tile_q0;
-    const uint32_t* __restrict__ tile_order;
-    int n, n_pad, u, sortidu, shortc;
-    double eps, eps2;
-};
+using Params = JoinParams;
 
 constexpr int kSmemDoubles = 4096;   // 32 KB candidate stage
 
@@ -278,16 +266,10 @@ int launch_np(const Params& p, JoinMode mode, const JoinArgs& a, bool sym, cudaS
 
 }  // namespace
 
-void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world, JoinArgs* a) {
-    // entity partitioning (§6.2): position j -> rank j mod |p|; batch (j div |p|) mod n_b
-    a->first = (int64_t)rank + (int64_t)world * batch;
-    a->step = (int64_t)world * n_batches;
-    a->n_tiles = a->first < ix->T ? (ix->T - a->first + a->step - 1) / a->step : 0;
-}
-
-int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
-    Params p;
+JoinParams join_params(const Index* ix) {
+    JoinParams p;
     p.pts = ix->pts;
+    p.pts32 = ix->pts32;
     p.orig = ix->orig;
     p.cell_start = ix->cell_start;
     p.nbr_off = ix->nbr_off;
@@ -303,6 +285,20 @@ int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t 
     p.shortc = ix->opt.shortc;
     p.eps = ix->eps;
     p.eps2 = ix->eps2;
+    p.thr32 = ix->thr32;
+    return p;
+}
+
+void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world, JoinArgs* a) {
+    // entity partitioning (§6.2): position j -> rank j mod |p|; batch (j div |p|) mod n_b
+    a->first = (int64_t)rank + (int64_t)world * batch;
+    a->step = (int64_t)world * n_batches;
+    a->n_tiles = a->first < ix->T ? (ix->T - a->first + a->step - 1) / a->step : 0;
+}
+
+int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
+    if (ix->fp32_filter && mode != kStats) return launch_join32(ix, mode, a, s);
+    const Params p = join_params(ix);
     const int np = ix->n_pad;
     const bool sym = ix->opt.symmetric != 0;
     if (np <= 8) return launch_np<8>(p, mode, a, sym, s);

@@ -1,0 +1,239 @@
+// SelfJoinKernel with a certified FP32 prefilter (B200-first variant of
+// PAPER.md Alg. 1 l.596-607; FP64 semantics unchanged).
+//
+// Same tiling as gj_join.cu (one CTA per 128-query tile of one cell, queries
+// in registers, candidates of each adjacent cell streamed through shared
+// memory, SORTIDU tile window, symmetric evaluation, warp-aggregated
+// emission), but the SHORTC scan runs on float32 copies of the centred
+// coordinates, fl32(x - min_j): the FP32 pipe has twice the FP64 pipe's lanes
+// on B200 and the stage holds twice the candidates.  A pair is rejected only
+// when its running FP32 sum exceeds thr32, which PROVES dist > eps (1 + 1e-9)
+// (derivation in gj_index.cu fp32_threshold and DESIGN.md); every pair that
+// survives all n dims is decided by the FP64 test, with exactly the FP64
+// kernel's arithmetic (FMA chain in dimension order).  The emitted pair set is
+// therefore the FP64 kernel's pair set, bit for bit.
+#include "gj_internal.cuh"
+
+namespace gj {
+namespace {
+
+constexpr int kSmemFloats = 8192;   // 32 KB candidate stage
+
+// FP64 decision of one pair: the FP64 kernel's arithmetic (gj_join.cu).
+__device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const double* __restrict__ b,
+                                             int n_pad) {
+    double acc = 0.0;
+    for (int d = 0; d < n_pad; d += 4) {
+        const double2 x = *reinterpret_cast<const double2*>(a + d);
+        const double2 y = *reinterpret_cast<const double2*>(a + d + 2);
+        const double2 u = *reinterpret_cast<const double2*>(b + d);
+        const double2 v = *reinterpret_cast<const double2*>(b + d + 2);
+        double t;
+        t = x.x - u.x; acc = fma(t, t, acc);
+        t = x.y - u.y; acc = fma(t, t, acc);
+        t = y.x - v.x; acc = fma(t, t, acc);
+        t = y.y - v.y; acc = fma(t, t, acc);
+    }
+    return acc;
+}
+
+template <int NPR, int MODE, bool SYM>
+__global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
+    constexpr int TC = kSmemFloats / NPR;   // candidates per stage (even)
+    __shared__ __align__(16) float Cs[kSmemFloats];
+    __shared__ uint32_t Cid[TC];
+    __shared__ uint32_t s_win[2];
+    __shared__ unsigned long long s_red[kTileQ / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t j = A.first + A.step * (int64_t)blockIdx.x;
+    const uint32_t tile = P.tile_order[j];
+    const uint32_t g = P.tile_cell[tile];
+    const uint32_t q0 = P.tile_q0[tile];
+    const uint32_t nq = min((uint32_t)kTileQ, P.cell_start[g + 1] - q0);
+    const bool active = tid < (int)nq;
+    const uint32_t qpos = q0 + (active ? tid : 0);
+    const int n_pad = P.n_pad;
+
+    float q[NPR];
+#pragma unroll
+    for (int d = 0; d < NPR; d += 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (d < n_pad) v = *reinterpret_cast<const float4*>(P.pts32 + (size_t)qpos * n_pad + d);
+        q[d] = v.x;
+        q[d + 1] = v.y;
+        q[d + 2] = v.z;
+        q[d + 3] = v.w;
+    }
+    const double eps = P.eps, eps2 = P.eps2;
+    const float thr = P.thr32;
+    const uint32_t qid = P.orig[qpos];
+    const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];
+    const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
+    const double* __restrict__ qrow64 = P.pts + (size_t)qpos * n_pad;
+    constexpr unsigned long long kMul = SYM ? 2ull : 1ull;
+
+    unsigned long long npairs = 0;
+    if (SYM) {   // the self pair (q, q)
+        if (MODE == kEmit) {
+            const unsigned m = __ballot_sync(0xffffffffu, active);
+            unsigned long long base = 0;
+            if (lane == 0 && m) base = atomicAdd((unsigned long long*)A.count, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (active) {
+                const unsigned long long at = base + __popc(m & lt);
+                if (at < A.cap) reinterpret_cast<uint2*>(A.out)[at] = make_uint2(qid, qid);
+            }
+        } else if (active) {
+            npairs += 1;
+        }
+    }
+
+    const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
+    for (uint32_t b = nb0; b < nb1; ++b) {
+        const uint32_t B = P.nbr[b];
+        uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
+        if (P.sortidu) {   // tile-level SORTIDU window (exact predicates on the fp64 u-coordinates)
+            __syncthreads();
+            if (tid < 2) {
+                uint32_t lo = r, hi = s;
+                while (lo < hi) {
+                    uint32_t mid = (lo + hi) >> 1;
+                    double cu = P.pts[(size_t)mid * n_pad + P.u];
+                    bool pred = tid == 0 ? (u_lo - cu <= eps) : (cu - u_hi > eps);
+                    if (pred) hi = mid; else lo = mid + 1;
+                }
+                s_win[tid] = lo;
+            }
+            __syncthreads();
+            r = s_win[0];
+            s = max(s_win[1], r);
+        }
+        const bool diag = SYM && B == g;
+        if (diag) r = max(r, q0 + 1);
+        for (uint32_t cb = r; cb < s; cb += TC) {
+            const int cntc = (int)min((uint32_t)TC, s - cb);
+            __syncthreads();
+            {
+                const float4* src = reinterpret_cast<const float4*>(P.pts32 + (size_t)cb * n_pad);
+                float4* dst = reinterpret_cast<float4*>(Cs);
+                const int nv = cntc * n_pad / 4;
+                for (int i = tid; i < nv; i += kTileQ) dst[i] = src[i];
+                for (int i = tid; i < cntc; i += kTileQ) Cid[i] = P.orig[cb + i];
+            }
+            __syncthreads();
+            for (int c = 0; c < cntc; c += 2) {
+                const bool two = c + 1 < cntc;
+                const float* cp0 = Cs + c * n_pad;
+                const float* cp1 = two ? cp0 + n_pad : cp0;
+                const uint32_t p0 = cb + c;
+                bool ok0 = active, ok1 = active && two;
+                if (diag) {
+                    ok0 = ok0 && p0 > qpos;
+                    ok1 = ok1 && p0 + 1 > qpos;
+                }
+                float a0 = ok0 ? 0.f : INFINITY, a1 = ok1 ? 0.f : INFINITY;
+                if (ok0 || ok1) {
+#pragma unroll
+                    for (int d = 0; d < NPR; d += 4) {
+                        if (d >= n_pad) break;
+                        const float4 x0 = *reinterpret_cast<const float4*>(cp0 + d);
+                        const float4 x1 = *reinterpret_cast<const float4*>(cp1 + d);
+                        float t;
+                        t = q[d] - x0.x;     a0 = fmaf(t, t, a0);
+                        t = q[d] - x1.x;     a1 = fmaf(t, t, a1);
+                        t = q[d + 1] - x0.y; a0 = fmaf(t, t, a0);
+                        t = q[d + 1] - x1.y; a1 = fmaf(t, t, a1);
+                        t = q[d + 2] - x0.z; a0 = fmaf(t, t, a0);
+                        t = q[d + 2] - x1.z; a1 = fmaf(t, t, a1);
+                        t = q[d + 3] - x0.w; a0 = fmaf(t, t, a0);
+                        t = q[d + 3] - x1.w; a1 = fmaf(t, t, a1);
+                        if ((d & 4) && P.shortc && a0 > thr && a1 > thr) break;   // SHORTC, every 8 dims
+                    }
+                }
+                // survivors of the prefilter: decided in FP64
+                bool hit0 = ok0 && a0 <= thr, hit1 = ok1 && a1 <= thr;
+                if (hit0) hit0 = dist2_fp64(qrow64, P.pts + (size_t)p0 * n_pad, n_pad) <= eps2;
+                if (hit1) hit1 = dist2_fp64(qrow64, P.pts + (size_t)(p0 + 1) * n_pad, n_pad) <= eps2;
+                if (MODE == kEmit) {
+                    const unsigned m0 = __ballot_sync(0xffffffffu, hit0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, hit1);
+                    if (m0 | m1) {
+                        const int leader = __ffs(m0 | m1) - 1;
+                        unsigned long long base = 0;
+                        if (lane == leader)
+                            base = atomicAdd((unsigned long long*)A.count, kMul * (__popc(m0) + __popc(m1)));
+                        base = __shfl_sync(0xffffffffu, base, leader);
+                        uint2* out = reinterpret_cast<uint2*>(A.out);
+                        if (hit0) {
+                            const unsigned long long at = base + kMul * __popc(m0 & lt);
+                            const uint32_t id = Cid[c];
+                            if (at + kMul <= A.cap) {
+                                out[at] = make_uint2(qid, id);
+                                if (SYM) out[at + 1] = make_uint2(id, qid);
+                            }
+                        }
+                        if (hit1) {
+                            const unsigned long long at = base + kMul * (__popc(m0) + __popc(m1 & lt));
+                            const uint32_t id = Cid[c + 1];
+                            if (at + kMul <= A.cap) {
+                                out[at] = make_uint2(qid, id);
+                                if (SYM) out[at + 1] = make_uint2(id, qid);
+                            }
+                        }
+                    }
+                } else {
+                    npairs += kMul * ((unsigned long long)hit0 + (unsigned long long)hit1);
+                }
+            }
+        }
+    }
+    if (MODE == kCount) {
+        unsigned long long x = npairs;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) s_red[tid >> 5] = x;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kTileQ / 32; ++w) t += s_red[w];
+            if (t) atomicAdd((unsigned long long*)A.count, t);
+            atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
+        }
+    }
+}
+
+template <int NPR>
+int launch32(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
+    if (a.n_tiles <= 0) return GJ_OK;
+    dim3 grid((unsigned)a.n_tiles);
+    if (mode == kEmit) {
+        if (sym) k_join32<NPR, kEmit, true><<<grid, kTileQ, 0, s>>>(p, a);
+        else k_join32<NPR, kEmit, false><<<grid, kTileQ, 0, s>>>(p, a);
+    } else {
+        if (sym) k_join32<NPR, kCount, true><<<grid, kTileQ, 0, s>>>(p, a);
+        else k_join32<NPR, kCount, false><<<grid, kTileQ, 0, s>>>(p, a);
+    }
+    count_launch();
+    GJ_CUDA(cudaGetLastError());
+    return GJ_OK;
+}
+
+}  // namespace
+
+int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
+    const JoinParams p = join_params(ix);
+    const int np = ix->n_pad;
+    const bool sym = ix->opt.symmetric != 0;
+    if (np <= 8) return launch32<8>(p, mode, a, sym, s);
+    if (np <= 16) return launch32<16>(p, mode, a, sym, s);
+    if (np <= 24) return launch32<24>(p, mode, a, sym, s);
+    if (np <= 32) return launch32<32>(p, mode, a, sym, s);
+    if (np <= 48) return launch32<48>(p, mode, a, sym, s);
+    if (np <= 64) return launch32<64>(p, mode, a, sym, s);
+    if (np <= 96) return launch32<96>(p, mode, a, sym, s);
+    return launch32<128>(p, mode, a, sym, s);
+}
+
+}  // namespace gj

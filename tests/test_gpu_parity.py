@@ -67,12 +67,49 @@ def test_pairs_equal_brute_force(gen, count, dims, eps, k):
     assert len(got) > count                       # real neighbours, not just self pairs
 
 
-@pytest.mark.parametrize("reorder,sortidu,shortc,symmetric",
-                         [(r, s, c, y) for r in (0, 1) for s in (0, 1) for c in (0, 1) for y in (0, 1)])
-def test_every_flag_combination(reorder, sortidu, shortc, symmetric):
+@pytest.mark.parametrize("reorder,sortidu,shortc,symmetric,fp32_filter",
+                         [(r, s, c, y, f) for r in (0, 1) for s in (0, 1) for c in (0, 1) for y in (0, 1)
+                          for f in (0, 1)])
+def test_every_flag_combination(reorder, sortidu, shortc, symmetric, fp32_filter):
     D = synth.exponential(2200, 24, seed=5)
-    got, _ = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc, symmetric=symmetric)
+    got, ix = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc, symmetric=symmetric,
+                        fp32_filter=fp32_filter)
+    assert ix.info().fp32_filter == fp32_filter
     check(D, 0.07, got)
+
+
+def _near_boundary_set(eps, n, m, rel, seed):
+    """m pairs of points at distance eps*(1 +/- rel) along random directions."""
+    rng = np.random.default_rng(seed)
+    base = rng.random((m, n)) * 0.5 + 0.25
+    dirs = rng.standard_normal((m, n))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    sign = np.where(np.arange(m) % 2 == 0, 1.0, -1.0)[:, None]
+    return np.concatenate([base, base + dirs * eps * (1 + sign * rel)])
+
+
+@pytest.mark.parametrize("rel", [1e-5, 1e-7, 3e-9])
+def test_fp32_prefilter_is_certified_near_the_boundary(rel):
+    # pairs just inside / just outside eps: the FP32 filter must never reject an
+    # inside pair, and both kernels must agree pair for pair.
+    eps, n = 0.05, 24
+    D = _near_boundary_set(eps, n, 3000, rel, seed=int(1 / rel) % 1000)
+    a, ix32 = gpu_pairs(D, eps, 3, fp32_filter=1)
+    b, _ = gpu_pairs(D, eps, 3, fp32_filter=0)
+    assert ix32.info().fp32_filter == 1
+    A = {tuple(r) for r in a.tolist()}
+    assert A == {tuple(r) for r in b.tolist()}
+    check(D, eps, a)
+
+
+def test_fp32_prefilter_switches_off_when_it_cannot_certify():
+    # huge coordinate spread relative to eps: the filter margin would exceed
+    # 1e-3 eps, so the index falls back to the FP64 scan (still exact).
+    D = synth.uniform(1500, 8, seed=3) * 1e7
+    D[:750, :] = D[:750, :] * 1e-7
+    got, ix = gpu_pairs(D, 0.05, 2, fp32_filter=1)
+    assert ix.info().fp32_filter == 0
+    check(D, 0.05, got)
 
 
 def test_lattice_exact_boundaries_are_inclusive():
