@@ -6,7 +6,9 @@
 // memory, SORTIDU tile window, symmetric evaluation, warp-aggregated
 // emission), but the SHORTC scan runs on float32 copies of the centred
 // coordinates, fl32(x - min_j): the FP32 pipe has twice the FP64 pipe's lanes
-// on B200 and the stage holds twice the candidates.  A pair is rejected only
+// on B200 and the stage holds twice the candidates.  Each thread tests its
+// query against two candidates at once with packed f32x2 adds / FMAs
+// (sm_100 FADD2/FFMA2), candidates staged pairwise interleaved and negated.  A pair is rejected only
 // when its running FP32 sum exceeds thr32, which PROVES dist > eps (1 + 1e-9)
 // (derivation in gj_index.cu fp32_threshold and DESIGN.md); every pair that
 // survives all n dims is decided by the FP64 test, with exactly the FP64
@@ -56,15 +58,17 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
     const uint32_t qpos = q0 + (active ? tid : 0);
     const int n_pad = P.n_pad;
 
-    float q[NPR];
+    // query coordinate d duplicated in both halves: operand of the packed
+    // f32x2 ops that test one query against two candidates at once
+    float2 q[NPR];
 #pragma unroll
     for (int d = 0; d < NPR; d += 4) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (d < n_pad) v = *reinterpret_cast<const float4*>(P.pts32 + (size_t)qpos * n_pad + d);
-        q[d] = v.x;
-        q[d + 1] = v.y;
-        q[d + 2] = v.z;
-        q[d + 3] = v.w;
+        q[d] = make_float2(v.x, v.x);
+        q[d + 1] = make_float2(v.y, v.y);
+        q[d + 2] = make_float2(v.z, v.z);
+        q[d + 3] = make_float2(v.w, v.w);
     }
     const double eps = P.eps, eps2 = P.eps2;
     const float thr = P.thr32;
@@ -116,42 +120,49 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
             const int cntc = (int)min((uint32_t)TC, s - cb);
             __syncthreads();
             {
-                const float4* src = reinterpret_cast<const float4*>(P.pts32 + (size_t)cb * n_pad);
-                float4* dst = reinterpret_cast<float4*>(Cs);
-                const int nv = cntc * n_pad / 4;
-                for (int i = tid; i < nv; i += kTileQ) dst[i] = src[i];
+                // stage candidate pairs (2p, 2p+1) interleaved and negated:
+                // Cs[p][d] = (-c_2p[d], -c_2p+1[d]) so that q - c is one f32x2 add
+                const float* src = P.pts32 + (size_t)cb * n_pad;
+                const int q4 = n_pad / 4;                      // float4 chunks per row
+                const int nv = ((cntc + 1) / 2) * q4;
+                for (int i = tid; i < nv; i += kTileQ) {
+                    const int pr = i / q4, d = (i - pr * q4) * 4;
+                    const float4 a = *reinterpret_cast<const float4*>(src + (size_t)(2 * pr) * n_pad + d);
+                    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (2 * pr + 1 < cntc) b = *reinterpret_cast<const float4*>(src + (size_t)(2 * pr + 1) * n_pad + d);
+                    float4* dst = reinterpret_cast<float4*>(Cs + (size_t)pr * 2 * n_pad + 2 * d);
+                    dst[0] = make_float4(-a.x, -b.x, -a.y, -b.y);
+                    dst[1] = make_float4(-a.z, -b.z, -a.w, -b.w);
+                }
                 for (int i = tid; i < cntc; i += kTileQ) Cid[i] = P.orig[cb + i];
             }
             __syncthreads();
             for (int c = 0; c < cntc; c += 2) {
                 const bool two = c + 1 < cntc;
-                const float* cp0 = Cs + c * n_pad;
-                const float* cp1 = two ? cp0 + n_pad : cp0;
+                const float* cp = Cs + (size_t)c * n_pad;     // pair c/2, interleaved
                 const uint32_t p0 = cb + c;
                 bool ok0 = active, ok1 = active && two;
                 if (diag) {
                     ok0 = ok0 && p0 > qpos;
                     ok1 = ok1 && p0 + 1 > qpos;
                 }
-                float a0 = ok0 ? 0.f : INFINITY, a1 = ok1 ? 0.f : INFINITY;
+                // a.x / a.y: running sums of candidates c / c+1; a dead one starts at +inf
+                float2 a = make_float2(ok0 ? 0.f : INFINITY, ok1 ? 0.f : INFINITY);
                 if (ok0 || ok1) {
 #pragma unroll
                     for (int d = 0; d < NPR; d += 4) {
                         if (d >= n_pad) break;
-                        const float4 x0 = *reinterpret_cast<const float4*>(cp0 + d);
-                        const float4 x1 = *reinterpret_cast<const float4*>(cp1 + d);
-                        float t;
-                        t = q[d] - x0.x;     a0 = fmaf(t, t, a0);
-                        t = q[d] - x1.x;     a1 = fmaf(t, t, a1);
-                        t = q[d + 1] - x0.y; a0 = fmaf(t, t, a0);
-                        t = q[d + 1] - x1.y; a1 = fmaf(t, t, a1);
-                        t = q[d + 2] - x0.z; a0 = fmaf(t, t, a0);
-                        t = q[d + 2] - x1.z; a1 = fmaf(t, t, a1);
-                        t = q[d + 3] - x0.w; a0 = fmaf(t, t, a0);
-                        t = q[d + 3] - x1.w; a1 = fmaf(t, t, a1);
-                        if ((d & 4) && P.shortc && a0 > thr && a1 > thr) break;   // SHORTC, every 8 dims
+                        const float4 x = *reinterpret_cast<const float4*>(cp + 2 * d);
+                        const float4 y = *reinterpret_cast<const float4*>(cp + 2 * d + 4);
+                        float2 t;
+                        t = __fadd2_rn(q[d], make_float2(x.x, x.y));     a = __ffma2_rn(t, t, a);
+                        t = __fadd2_rn(q[d + 1], make_float2(x.z, x.w)); a = __ffma2_rn(t, t, a);
+                        t = __fadd2_rn(q[d + 2], make_float2(y.x, y.y)); a = __ffma2_rn(t, t, a);
+                        t = __fadd2_rn(q[d + 3], make_float2(y.z, y.w)); a = __ffma2_rn(t, t, a);
+                        if ((d & 4) && P.shortc && a.x > thr && a.y > thr) break;   // SHORTC, every 8 dims
                     }
                 }
+                const float a0 = a.x, a1 = a.y;
                 // survivors of the prefilter: decided in FP64
                 bool hit0 = ok0 && a0 <= thr, hit1 = ok1 && a1 <= thr;
                 if (hit0) hit0 = dist2_fp64(qrow64, P.pts + (size_t)p0 * n_pad, n_pad) <= eps2;
