@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=24, help="oracle query sample for cpu_baseline")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu baseline/clocks")
+    p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo lets several ranks share one GPU "
+                   "to exercise the multi-rank path on a 1-GPU box")
     return p.parse_args()
 
 
@@ -174,9 +176,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     w = workload(args)
@@ -195,14 +201,24 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if args.dist_backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
-    def one_step(out, cnt, ev_join):
-        """The timed hot path; returns (index, pairs of this rank, join events)."""
+    def one_step(out, cnt, ev_join, ev_phase=None):
+        """The timed hot path; returns (index, n_b).  ev_join brackets the join
+        kernels; ev_phase (optional) = [after broadcast, after build, after estimate]."""
         if world > 1:
             dist.broadcast(D_dev, src=0)
+        if ev_phase:
+            ev_phase[0].record(stream)
         ix = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
+        if ev_phase:
+            ev_phase[1].record(stream)
         est = ix.estimate(0.01, rank, world)
+        if ev_phase:
+            ev_phase[2].record(stream)
         nb = num_batches(est, args.batch_size)
         cnt.zero_()
         ev_join[0].record(stream)
@@ -225,7 +241,7 @@ def main():
     cap = int(exact * 1.02) + 65536
     out = torch.empty((cap, 2), dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     # L2 hygiene: the point array (N*n*8 bytes) and the index are re-built every
     # step; an extra 256 MB flush buffer is written between timed steps.
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
@@ -236,18 +252,20 @@ def main():
         ix.free()
     launches0 = gpujoin.launch_count()
     clocks = Clocks(local).start() if not args.profile else None
-    step_ms, join_ms, pairs = [], [], 0
+    step_ms, join_ms, phase_ms, pairs = [], [], [], 0
     for _ in range(args.steps):
         flush.fill_(1)
         barrier()
         torch.cuda.synchronize()
         ev[0].record(stream)
-        ix, nb = one_step(out, cnt, ev[2:4])
+        ix, nb = one_step(out, cnt, ev[2:4], ev[4:7])
         ev[1].record(stream)
         torch.cuda.synchronize()
         barrier()
         step_ms.append(ev[0].elapsed_time(ev[1]))
         join_ms.append(ev[2].elapsed_time(ev[3]))
+        phase_ms.append([ev[0].elapsed_time(ev[4]), ev[4].elapsed_time(ev[5]), ev[5].elapsed_time(ev[6]),
+                         ev[6].elapsed_time(ev[2])])
         got = int(cnt.item())
         if got > cap:
             raise RuntimeError(f"result buffer overflow {got} > {cap}")
@@ -344,6 +362,8 @@ def main():
         "join_time_s": ms / 1000.0, "pairs": total_pairs, "selectivity": (total_pairs - N) / N,
         "index": {"n_cells": info.n_cells, "n_adjacent": info.n_adjacent, "n_tiles": info.n_tiles,
                   "est_candidates": info.est_candidates},
+        "phases_ms": dict(zip(["broadcast", "build_index", "estimate", "plan", "join"],
+                              [float(np.mean([p[i] for p in phase_ms])) for i in range(4)] + [jms])),
         "gpu_launches": int(launches), "e2e": e2e, "roofline": roof, "clocks": clk,
     }
     if not args.no_cpu_baseline and not args.profile:

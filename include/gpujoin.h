@@ -123,6 +123,14 @@ GJ_API int gj_device_arrays(const gj_index* idx, const double** points_sorted, c
  * sampled query fraction.  Returns estimated pairs of this rank's share. */
 GJ_API int gj_estimate(gj_index* idx, double frac, int32_t rank, int32_t world, int64_t* est_pairs);
 
+/* Host only: rejection threshold of the certified FP32 prefilter for radius
+ * eps and per-dimension spans s_j = max_j - min_j (n values).  A pair whose
+ * float32 running sum of fl32(fl32(q_j - min_j) - fl32(c_j - min_j))^2 (FMA
+ * accumulation, any prefix of the dims) exceeds *thr is provably farther than
+ * eps (1 + 1e-9).  *margin = thr / eps^2 - 1 (from the exact double value).
+ * Returns 1 if the filter is enabled for such data, 0 if not, <0 on error. */
+GJ_API int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, double* margin);
+
 /* computeNumBatches (§3.2.2 l.199-200): n_b = max(3, ceil(est / batch_size)). */
 GJ_API int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size);
 

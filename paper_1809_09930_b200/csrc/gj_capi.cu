@@ -204,6 +204,11 @@ int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, in
     return GJ_OK;
 }
 
+int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, double* margin) {
+    if (!spans || !thr || !margin || n < 1 || n > kMaxDim || !(eps > 0.0)) { set_error("bad argument"); return GJ_ERR_INVALID; }
+    return fp32_threshold_from_spans(eps, n, spans, thr, margin);
+}
+
 int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size) {
     if (batch_size <= 0) batch_size = 100000000ll;
     int64_t nb = (std::max<int64_t>(est_pairs, 0) + batch_size - 1) / batch_size;

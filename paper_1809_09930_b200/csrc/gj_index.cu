@@ -341,27 +341,32 @@ inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) /
 // the pair is outside eps and outside the 1e-12 ambiguity band.  Every pair the
 // filter does not reject is decided by the FP64 test.  The filter is switched
 // off when it could not reject much (A > 1e-3 eps) or fp32 could overflow.
-void fp32_threshold(Index* ix) {
-    const Meta& m = ix->h_meta;
+}  // namespace
+
+int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr, double* margin) {
     double ss = 0.0, smax = 0.0;
-    for (int t = 0; t < ix->n; ++t) {
-        const int o = m.order[t];
-        const double sj = m.maxs[o] - m.mins[o];
-        ss += sj * sj;
-        smax = std::max(smax, sj);
+    for (int t = 0; t < n; ++t) {
+        ss += spans[t] * spans[t];
+        smax = std::max(smax, spans[t]);
     }
     const double u = std::ldexp(1.0, -24);
-    const double A = 4.001 * u * std::sqrt(ss) * (1.0 + 1e-12) + std::sqrt((double)ix->n) * std::ldexp(1.0, -147);
-    const double gamma = ix->n * u / (1.0 - ix->n * u);
-    const double T = (1.0 + gamma) * (ix->eps * (1.0 + 1e-9) + A) * (ix->eps * (1.0 + 1e-9) + A);
+    const double A = 4.001 * u * std::sqrt(ss) * (1.0 + 1e-12) + std::sqrt((double)n) * std::ldexp(1.0, -147);
+    const double gamma = n * u / (1.0 - n * u);
+    const double T = (1.0 + gamma) * (eps * (1.0 + 1e-9) + A) * (eps * (1.0 + 1e-9) + A);
     float T32 = (float)T;
     if ((double)T32 < T) T32 = std::nextafter(T32, INFINITY);
-    ix->filter_margin = T / (ix->eps * ix->eps) - 1.0;
-    ix->thr32 = T32;
-    if (!(smax < 1e30) || !(T32 < 1e30f) || A > 1e-3 * ix->eps) ix->fp32_filter = 0;
+    *margin = T / (eps * eps) - 1.0;
+    *thr = T32;
+    return (smax < 1e30) && (T32 < 1e30f) && !(A > 1e-3 * eps);
 }
 
-}  // namespace
+static void fp32_threshold(Index* ix) {
+    const Meta& m = ix->h_meta;
+    double spans[kMaxDim];
+    for (int t = 0; t < ix->n; ++t) spans[t] = m.maxs[m.order[t]] - m.mins[m.order[t]];
+    if (!fp32_threshold_from_spans(ix->eps, ix->n, spans, &ix->thr32, &ix->filter_margin)) ix->fp32_filter = 0;
+}
+
 
 int build_index(Index* ix, const double* X) {
     cudaStream_t s = ix->stream;

@@ -84,6 +84,9 @@ int radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, uint64_t bits_mask
 int varying_bits_u64(const uint64_t* keys, int64_t n, uint64_t* h_out, cudaStream_t s);
 
 // ---- index build (gj_index.cu) ----
+// Certified FP32 prefilter threshold from the per-dim spans (max - min);
+// returns 0 when the filter cannot be certified usefully.
+int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr, double* margin);
 int build_index(Index* ix, const double* d_points);
 
 // ---- join (gj_join.cu) ----

@@ -41,7 +41,7 @@ __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const
 
 template <int NPR, int MODE, bool SYM>
 __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
-    constexpr int TC = kSmemFloats / NPR;   // candidates per stage (even)
+    constexpr int TC = (kSmemFloats / NPR) & ~1;   // candidates per stage (even: staged in pairs)
     __shared__ __align__(16) float Cs[kSmemFloats];
     __shared__ uint32_t Cid[TC];
     __shared__ uint32_t s_win[2];

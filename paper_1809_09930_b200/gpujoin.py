@@ -19,7 +19,7 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 
 # Every symbol include/gpujoin.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
-           "gj_estimate", "gj_num_batches", "gj_partition", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
+           "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
            "gj_self_join_host", "gj_join_stats", "gj_neighbor_table", "gj_free_index", "gj_last_error",
            "gj_abi_version", "gj_launch_count"]
 
@@ -68,6 +68,7 @@ def lib():
         "gj_device_arrays": (C.c_int, [P, C.POINTER(P), C.POINTER(P)]),
         "gj_estimate": (C.c_int, [P, D, I32, I32, C.POINTER(I64)]),
         "gj_num_batches": (I64, [I64, I64]),
+        "gj_fp32_threshold": (C.c_int, [D, I32, C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(D)]),
         "gj_partition": (C.c_int, [I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
         "gj_self_join_async": (C.c_int, [P, P, I64, P, I32, I32, I32, I32]),
         "gj_self_join_count_async": (C.c_int, [P, P, I32, I32, I32, I32]),
@@ -233,6 +234,17 @@ def partition(n_tiles: int, rank: int, world: int, batch: int = 0, n_batches: in
     f, s, c = C.c_int64(), C.c_int64(), C.c_int64()
     _check(lib().gj_partition(int(n_tiles), rank, world, batch, n_batches, C.byref(f), C.byref(s), C.byref(c)))
     return f.value, s.value, c.value
+
+
+def fp32_threshold(eps: float, spans):
+    """(enabled, threshold float32, margin) of the certified FP32 prefilter."""
+    sp = np.ascontiguousarray(spans, dtype=np.float64)
+    t, m = C.c_float(), C.c_double()
+    rc = lib().gj_fp32_threshold(float(eps), len(sp), sp.ctypes.data_as(C.POINTER(C.c_double)), C.byref(t),
+                                 C.byref(m))
+    if rc < 0:
+        _check(rc)
+    return bool(rc), np.float32(t.value), m.value
 
 
 def launch_count() -> int:

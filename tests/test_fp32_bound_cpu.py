@@ -1,0 +1,75 @@
+"""CPU check of the certified FP32 prefilter bound (gj_fp32_threshold;
+DESIGN.md §"FP32 prefilter"): the kernel's float32 arithmetic is emulated
+exactly (correctly rounded float32 conversions, adds and FMAs via exact
+rationals) on adversarial pairs whose exact distance is at or just inside
+eps; none may have a float32 running sum above the threshold, at any prefix.
+Also checks the threshold stays within a small relative margin of eps^2."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from paper_1809_09930_b200 import gpujoin
+
+
+def f32(fr: Fraction) -> Fraction:
+    """Correctly rounded (nearest, ties to even) float32 of an exact rational."""
+    x = np.float32(float(fr))
+    best = None
+    for c in (np.nextafter(x, np.float32(-np.inf)), x, np.nextafter(x, np.float32(np.inf))):
+        d = abs(Fraction(float(c)) - fr)
+        key = (d, int(np.frombuffer(np.float32(c).tobytes(), np.uint32)[0]) & 1)
+        if best is None or key < best[0]:
+            best = (key, c)
+    return Fraction(float(best[1]))
+
+
+def kernel_sums(q, c, mins):
+    """Running float32 sums exactly as k_join32 computes them."""
+    a = Fraction(0)
+    out = []
+    for j in range(len(q)):
+        qj = f32(Fraction(float(np.float64(q[j]) - np.float64(mins[j]))))    # fl32(fl64(q - min))
+        cj = f32(Fraction(float(np.float64(c[j]) - np.float64(mins[j]))))
+        t = f32(qj - cj)                                                   # FADD2 (q + (-c))
+        a = f32(t * t + a)                                                 # FFMA2, one rounding
+        out.append(a)
+    return out
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+@pytest.mark.parametrize("n,eps,span,shift", [(8, 0.05, 1.0, 0.0), (16, 0.3, 2.0, -1.0), (32, 0.08, 1.0, 0.0),
+                                              (24, 1e-2, 1.0, 1000.0), (24, 1e-3, 1.0, 1000.0)])
+def test_no_inside_pair_is_rejected(n, eps, span, shift):
+    rng = np.random.default_rng(n)
+    mins = np.full(n, shift)
+    enabled, thr, margin = gpujoin.fp32_threshold(eps, np.full(n, span))
+    assert margin > 0
+    if not enabled:
+        assert margin > 1e-3
+        pytest.skip("filter disabled for this spread")
+    thr = Fraction(float(thr))
+    for _ in range(300):
+        q = shift + rng.random(n) * span
+        v = rng.standard_normal(n)
+        v /= np.linalg.norm(v)
+        r = eps * (1 - rng.random() * 1e-7)                  # exact distance at/just inside eps
+        c = q + v * r
+        c = np.clip(c, shift, shift + span)
+        d2 = sum((Fraction(float(a)) - Fraction(float(b))) ** 2 for a, b in zip(q, c))
+        if d2 > Fraction(eps) ** 2:
+            continue
+        for s in kernel_sums(q, c, mins):
+            assert s <= thr
+
+
+def test_threshold_margin_and_switch_off():
+    on, thr, margin = gpujoin.fp32_threshold(0.08, np.full(32, 0.4))
+    assert on and 0 < margin < 1e-4 and float(thr) >= 0.08 ** 2
+    off, _, _ = gpujoin.fp32_threshold(1e-6, np.full(32, 1e3))     # A > 1e-3 eps -> disabled
+    assert not off
