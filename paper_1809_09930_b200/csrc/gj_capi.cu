@@ -250,6 +250,9 @@ int gj_estimate(gj_index* h, double frac, int32_t rank, int32_t world, int64_t* 
     a.first = rank;
     a.step = (int64_t)world * stepf;
     a.n_tiles = a.first < ix.T ? (ix.T - a.first + a.step - 1) / a.step : 0;
+    // a 1% sample of tiles is far too few CTAs to fill 148 SMs: split every
+    // sampled tile's candidate scan over enough CTAs for ~8 waves of 148
+    a.split = (int32_t)std::max<int64_t>(1, std::min<int64_t>(64, (8 * 148 + a.n_tiles - 1) / std::max<int64_t>(1, a.n_tiles)));
     GJ_CUDA(cudaMemsetAsync(ix.scratch_count, 0, 8 * sizeof(uint64_t), s));
     if (int rc = launch_join(&ix, kCount, a, s)) return rc;
     // queries of the whole share

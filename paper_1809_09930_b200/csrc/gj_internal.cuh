@@ -98,6 +98,7 @@ struct JoinArgs {
     int64_t first;            // first tile position j
     int64_t step;             // tile positions j = first + step * m
     int64_t n_tiles;          // number of m values
+    int32_t split;            // CTAs per tile, each scanning 1/split of every candidate window (0/1 = none)
 };
 struct JoinParams {
     const double* __restrict__ pts;

@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
 
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t j = A.first + A.step * (int64_t)blockIdx.x;
+    // split-K over candidates: CTA (m, part) scans part `part` of every window
+    const int split = A.split > 1 ? A.split : 1;
+    const int part = (int)(blockIdx.x % split);
+    const int64_t j = A.first + A.step * (int64_t)(blockIdx.x / split);
     const uint32_t tile = P.tile_order[j];
     const uint32_t g = P.tile_cell[tile];
     const uint32_t q0 = P.tile_q0[tile];
@@ -87,8 +90,8 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     constexpr unsigned long long kMul = SYM ? 2ull : 1ull;   // ordered pairs per evaluated pair
 
     unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
-    if (MODE == kStats && active) cnt[1] += P.nbr_off[g + 1] - P.nbr_off[g];
-    if (SYM) {   // the self pair (q, q): d = 0 <= eps
+    if (MODE == kStats && active && part == 0) cnt[1] += P.nbr_off[g + 1] - P.nbr_off[g];
+    if (SYM && part == 0) {   // the self pair (q, q): d = 0 <= eps
         if (MODE == kEmit) {
             const unsigned m = __ballot_sync(0xffffffffu, active);
             unsigned long long base = 0;
@@ -127,6 +130,11 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
         }
         const bool diag = SYM && B == g;
         if (diag) r = max(r, q0 + 1);   // own cell: only candidates after the query
+        if (split > 1 && s > r) {
+            const uint64_t len = s - r;
+            s = r + (uint32_t)(len * (part + 1) / split);
+            r = r + (uint32_t)(len * part / split);
+        }
         for (uint32_t cb = r; cb < s; cb += TC) {
             const int cntc = (int)min((uint32_t)TC, s - cb);
             __syncthreads();
@@ -242,13 +250,14 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
             for (int w = 0; w < kTileQ / 32; ++w) t += s_red[tid][w];
             if (t) atomicAdd((unsigned long long*)A.count + tid, t);
         }
-        if (MODE == kCount && tid == 0) atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
+        if (MODE == kCount && tid == 0 && part == 0)
+            atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
     }
 }
 
 template <int NPR, bool SYM>
 void launch_mode(const Params& p, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
-    dim3 grid((unsigned)a.n_tiles);
+    dim3 grid((unsigned)(a.n_tiles * (a.split > 1 ? a.split : 1)));
     if (mode == kEmit) k_join<NPR, kEmit, SYM><<<grid, kTileQ, 0, s>>>(p, a);
     else if (mode == kCount) k_join<NPR, kCount, SYM><<<grid, kTileQ, 0, s>>>(p, a);
     else k_join<NPR, kStats, SYM><<<grid, kTileQ, 0, s>>>(p, a);

@@ -49,7 +49,10 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
 
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t j = A.first + A.step * (int64_t)blockIdx.x;
+    // split-K over candidates: CTA (m, part) scans part `part` of every window
+    const int split = A.split > 1 ? A.split : 1;
+    const int part = (int)(blockIdx.x % split);
+    const int64_t j = A.first + A.step * (int64_t)(blockIdx.x / split);
     const uint32_t tile = P.tile_order[j];
     const uint32_t g = P.tile_cell[tile];
     const uint32_t q0 = P.tile_q0[tile];
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
     constexpr unsigned long long kMul = SYM ? 2ull : 1ull;
 
     unsigned long long npairs = 0;
-    if (SYM) {   // the self pair (q, q)
+    if (SYM && part == 0) {   // the self pair (q, q)
         if (MODE == kEmit) {
             const unsigned m = __ballot_sync(0xffffffffu, active);
             unsigned long long base = 0;
@@ -116,6 +119,11 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
         }
         const bool diag = SYM && B == g;
         if (diag) r = max(r, q0 + 1);
+        if (split > 1 && s > r) {
+            const uint64_t len = s - r;
+            s = r + (uint32_t)(len * (part + 1) / split);
+            r = r + (uint32_t)(len * part / split);
+        }
         for (uint32_t cb = r; cb < s; cb += TC) {
             const int cntc = (int)min((uint32_t)TC, s - cb);
             __syncthreads();
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
             unsigned long long t = 0;
             for (int w = 0; w < kTileQ / 32; ++w) t += s_red[w];
             if (t) atomicAdd((unsigned long long*)A.count, t);
-            atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
+            if (part == 0) atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
         }
     }
 }
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
 template <int NPR>
 int launch32(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
-    dim3 grid((unsigned)a.n_tiles);
+    dim3 grid((unsigned)(a.n_tiles * (a.split > 1 ? a.split : 1)));
     if (mode == kEmit) {
         if (sym) k_join32<NPR, kEmit, true><<<grid, kTileQ, 0, s>>>(p, a);
         else k_join32<NPR, kEmit, false><<<grid, kTileQ, 0, s>>>(p, a);
