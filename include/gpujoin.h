@@ -51,7 +51,7 @@ extern "C" {
 typedef struct gj_index gj_index; /* opaque handle */
 
 /* Options of Algorithm 1.  Zero-initialise then set fields; gj_default_options fills them
- * (reorder = sortidu = shortc = symmetric = fp32_filter = 1, sample_frac = 0.01, stream = 0). */
+ * (reorder = sortidu = shortc = symmetric = 1, filter = 2, sample_frac = 0.01, stream = 0). */
 typedef struct {
     int32_t reorder;     /* 1: REORDER dims by variance (§4.2); 0: index the first k dims */
     int32_t sortidu;     /* 1: SORTIDU prune on the un-indexed dim u (§4.3)               */
@@ -60,8 +60,14 @@ typedef struct {
                             0: one full neighbour search per query (Alg. 1 verbatim)        */
     double sample_frac;  /* variance sample fraction (§4.2 "1% of |D|"), in (0,1]        */
     uint64_t stream;     /* cudaStream_t the index issues its work on                     */
-    int32_t fp32_filter; /* 1: certified FP32 prefilter, every surviving pair decided in FP64
-                            (same pair set as 0 = FP64 scan); ignored by gj_join_stats      */
+    int32_t filter;      /* candidate filter of the join kernel; every pair it cannot reject is
+                            decided by the FP64 test, so the pair set is the same for all:
+                            0 = FP64 SHORTC scan (Alg. 1 verbatim arithmetic)
+                            1 = certified FP32 SHORTC prefilter (SIMT, packed f32x2)
+                            2 = certified tensor-core bound (fp16 MMA, fp32 accumulate) on
+                                dense cell-pair blocks (default); falls back to 1, then 0,
+                                when the data's spread makes the bound uncertifiable.
+                            gj_join_stats always runs the FP64 scan.                          */
     int32_t reserved1;
 } gj_options;
 
@@ -78,9 +84,9 @@ typedef struct {
     int64_t n_tiles;      /* query tiles (<= 128 queries of one cell each)         */
     double est_candidates;/* sum over queries of candidates before SORTIDU         */
     double build_ms;      /* device time of gj_build_index (CUDA events)           */
-    int32_t fp32_filter;  /* 1 if the join kernel runs the certified FP32 prefilter */
-    float filter_threshold;  /* its rejection threshold on the FP32 running sum    */
-    double filter_margin; /* filter_threshold / eps^2 - 1                           */
+    int32_t filter;       /* filter the join kernel actually runs (0/1/2, see gj_options) */
+    float filter_threshold;  /* its rejection threshold (filter 2: in scaled units)      */
+    double filter_margin; /* threshold / eps^2 - 1 (relative slack of the bound)          */
 } gj_info;
 
 /* Work counters of one join (gj_join_stats).  cells/tests/dims/pairs are the

@@ -104,7 +104,7 @@ void gj_default_options(gj_options* opt) {
     opt->sortidu = 1;
     opt->shortc = 1;
     opt->symmetric = 1;
-    opt->fp32_filter = 1;
+    opt->filter = 2;
     opt->sample_frac = 0.01;
 }
 
@@ -131,7 +131,8 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     ix.eps2 = eps * eps;
     ix.opt = o;
     ix.stream = (cudaStream_t)o.stream;
-    ix.fp32_filter = o.fp32_filter ? 1 : 0;
+    if (o.filter < 0 || o.filter > 2) { set_error("filter must be 0, 1 or 2"); delete h; return GJ_ERR_INVALID; }
+    ix.filter = o.filter;
     const double* dX = points;
     double* staged = nullptr;
     int rc = GJ_OK;
@@ -170,9 +171,9 @@ int gj_index_info(const gj_index* h, gj_info* info) {
     info->n_tiles = ix.T;
     info->est_candidates = ix.est_candidates;
     info->build_ms = ix.build_ms;
-    info->fp32_filter = ix.fp32_filter;
-    info->filter_threshold = ix.thr32;
-    info->filter_margin = ix.filter_margin;
+    info->filter = ix.filter;
+    info->filter_threshold = ix.filter == 2 ? ix.thr16 : ix.thr32;
+    info->filter_margin = ix.filter == 2 ? ix.margin16 : ix.filter_margin;
     return GJ_OK;
 }
 
@@ -453,7 +454,7 @@ void gj_free_index(gj_index* h) {
     if (!h) return;
     Index& ix = h->ix;
     cudaStreamSynchronize(ix.stream);
-    void* ptrs[] = {ix.pts, ix.pts32, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
+    void* ptrs[] = {ix.pts, ix.pts32, ix.pts16, ix.norm16, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
                     ix.tile_order, ix.tile_work, ix.meta, ix.scratch_count};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -18,6 +18,7 @@
 // R6 sample = every round(1/f)-th point, unbiased variance, ties -> lower dim;
 // R7 u = position k if k < n else 0; R9 first indexed dim most significant.
 #include <math.h>
+#include <string.h>
 
 #include <cmath>
 
@@ -360,11 +361,104 @@ int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr
     return (smax < 1e30) && (T32 < 1e30f) && !(A > 1e-3 * eps);
 }
 
-static void fp32_threshold(Index* ix) {
+static bool fp32_threshold(Index* ix) {
     const Meta& m = ix->h_meta;
     double spans[kMaxDim];
     for (int t = 0; t < ix->n; ++t) spans[t] = m.maxs[m.order[t]] - m.mins[m.order[t]];
-    if (!fp32_threshold_from_spans(ix->eps, ix->n, spans, &ix->thr32, &ix->filter_margin)) ix->fp32_filter = 0;
+    return fp32_threshold_from_spans(ix->eps, ix->n, spans, &ix->thr32, &ix->filter_margin) != 0;
+}
+
+// Threshold of the certified tensor-core bound (gj_join_tc.cu; DESIGN.md
+// §"Tensor-core bound").  Scaled, centred fp16 operands x^ = fp16(S (x - min)),
+// R2 = max ||x^||^2, K = padded MMA depth.  The kernel rejects a pair when
+// v = fl32(||c^||^2 - 2 acc) > fl32(thr - ||q^||^2), acc = the tensor-core fp32
+// accumulation of q^.c^.  Error terms (all conservative):
+//   delta : | ||q^ - c^|| - S||q - c|| | <= 2^-11 (||q'|| + ||c'||) + sqrt(n) 2^-24
+//   kappa : |acc - q^.c^| <= kappa R2, kappa = (K + 2) 2^-21 (4x a truncating fp32 adder)
+//   E1    : 2 kappa R2 + 4 R2 2^-24          (accumulation, v and norm roundings)
+//   E2    : 2^-23 (T0 + R2) * 1.01           (rounding of thr - ||q^||^2)
+// T = (S eps (1 + 1e-9) + delta)^2 + E1 + E2  =>  v > fl32(T - ||q^||^2) implies
+// ||q - c|| > eps (1 + 1e-9).  Enabled when the relative slack T/(S eps)^2 - 1 < 0.25.
+int tc_threshold_from(double eps, int n, int K, double S, double R2, float* thr, double* margin) {
+    const double R = std::sqrt(R2);
+    const double Rp = (R + std::sqrt((double)n) * std::ldexp(1.0, -25)) / (1.0 - std::ldexp(1.0, -11));
+    const double delta = std::ldexp(1.0, -11) * 2.0 * Rp + std::sqrt((double)n) * std::ldexp(1.0, -24);
+    const double kappa = (K + 2) * std::ldexp(1.0, -21);
+    const double E1 = 2.0 * kappa * R2 + 4.0 * R2 * std::ldexp(1.0, -24);
+    const double epsS = S * eps * (1.0 + 1e-9);
+    const double T0 = (epsS + delta) * (epsS + delta) + E1;
+    const double E2 = std::ldexp(1.0, -23) * (T0 + R2) * 1.01;
+    const double T = T0 + E2;
+    float T32 = (float)T;
+    if ((double)T32 < T) T32 = std::nextafter(T32, INFINITY);
+    *thr = T32;
+    *margin = T / ((S * eps) * (S * eps)) - 1.0;
+    return std::isfinite(T) && T32 < 1e30f && *margin < 0.25;
+}
+
+namespace {
+// pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond; norm16[p] =
+// ||pts16[p]||^2 (fp64 sum, rounded to fp32); R2 = max over p (exact doubles).
+__global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, int k16, double S,
+                         const Meta* __restrict__ meta, __half* __restrict__ pts16, float* __restrict__ norm16,
+                         unsigned long long* __restrict__ r2max) {
+    __shared__ double mn[kMaxDim];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) mn[t] = meta->mins[meta->order[t]];
+    __syncthreads();
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double nrm = 0.0;
+    if (p < N) {
+        for (int t = 0; t < k16; ++t) {
+            __half h = __float2half(0.f);
+            if (t < n) h = __double2half(S * (pts[p * n_pad + t] - mn[t]));
+            pts16[p * k16 + t] = h;
+            const double hd = (double)__half2float(h);
+            nrm += hd * hd;
+        }
+        norm16[p] = (float)nrm;
+    }
+    // block max of the (non-negative) norms via their ordered bit patterns
+    unsigned long long bits = (unsigned long long)__double_as_longlong(nrm);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(r2max, bits);
+}
+}  // namespace
+
+// Builds the fp16 operands; returns true if the tensor-core bound is certified.
+static int make_fp16(Index* ix, bool* ok) {
+    cudaStream_t s = ix->stream;
+    const Meta& m = ix->h_meta;
+    double smax = 0.0;
+    for (int t = 0; t < ix->n; ++t) smax = std::max(smax, m.maxs[m.order[t]] - m.mins[m.order[t]]);
+    *ok = false;
+    if (!(smax < 1e300)) return GJ_OK;
+    // S: power of two putting the largest centred coordinate in [2^13, 2^14)
+    ix->tc_scale = smax > 0.0 ? std::ldexp(1.0, (int)std::floor(std::log2(16384.0 / smax))) : 1.0;
+    ix->k16 = (ix->n + 15) & ~15;
+    const int64_t N = ix->N;
+    GJ_CUDA(cudaMallocAsync(&ix->pts16, (size_t)N * ix->k16 * sizeof(__half), s));
+    GJ_CUDA(cudaMallocAsync(&ix->norm16, (size_t)N * sizeof(float), s));
+    unsigned long long* d_r2 = nullptr;
+    GJ_CUDA(cudaMallocAsync(&d_r2, sizeof(*d_r2), s));
+    GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
+    k_make16<<<blocks_for(N, 256), 256, 0, s>>>(ix->pts, N, ix->n, ix->n_pad, ix->k16, ix->tc_scale, ix->meta,
+                                                 ix->pts16, ix->norm16, d_r2); count_launch();
+    GJ_CUDA(cudaGetLastError());
+    unsigned long long h_r2 = 0;
+    GJ_CUDA(cudaMemcpyAsync(&h_r2, d_r2, sizeof(h_r2), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaFreeAsync(d_r2, s));
+    GJ_CUDA(cudaStreamSynchronize(s));
+    double R2;
+    memcpy(&R2, &h_r2, sizeof(R2));
+    *ok = tc_threshold_from(ix->eps, ix->n, ix->k16, ix->tc_scale, R2, &ix->thr16, &ix->margin16) != 0;
+    if (!*ok) {
+        GJ_CUDA(cudaFreeAsync(ix->pts16, s));
+        GJ_CUDA(cudaFreeAsync(ix->norm16, s));
+        ix->pts16 = nullptr;
+        ix->norm16 = nullptr;
+    }
+    return GJ_OK;
 }
 
 
@@ -399,7 +493,8 @@ int build_index(Index* ix, const double* X) {
         set_error("linearized cell id needs >= 2^63 cells (prod of per-dim widths); choose a smaller k");
         return GJ_ERR_OVERFLOW;
     }
-    fp32_threshold(ix);
+    const bool fp32_ok = fp32_threshold(ix);
+    const bool want32 = ix->filter >= 1 && fp32_ok;
     // 3. keys
     uint64_t *cellkey = nullptr, *ukey = nullptr, *tmp64 = nullptr;
     uint32_t* idx = nullptr;
@@ -422,9 +517,16 @@ int build_index(Index* ix, const double* X) {
     // 5. sorted, reordered point array
     GJ_CUDA(cudaMallocAsync(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
     GJ_CUDA(cudaMallocAsync(&ix->orig, N * sizeof(uint32_t), s));
-    if (ix->fp32_filter) GJ_CUDA(cudaMallocAsync(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
+    if (want32) GJ_CUDA(cudaMallocAsync(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
     k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, ix->pts32); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    if (ix->filter == 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
+        bool tc_ok = false;
+        if ((rc = make_fp16(ix, &tc_ok))) return rc;
+        if (!tc_ok) ix->filter = want32 ? 1 : 0;
+    } else if (ix->filter == 1 && !want32) {
+        ix->filter = 0;
+    }
     // 6. non-empty cells
     uint32_t *head = nullptr, *pos = nullptr, *d_tot = nullptr;
     GJ_CUDA(cudaMallocAsync(&head, N * sizeof(uint32_t), s));

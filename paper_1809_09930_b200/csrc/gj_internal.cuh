@@ -1,5 +1,6 @@
 // Internal declarations shared by the CUDA translation units of libgpujoin.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -51,9 +52,15 @@ struct Index {
     // device arrays
     double* pts = nullptr;           // [N][n_pad] reordered dims, sorted by (cell, u)
     float* pts32 = nullptr;          // [N][n_pad] fl32(x - min_j): input of the certified FP32 prefilter
-    int fp32_filter = 0;             // 1: join kernel runs the FP32 prefilter + FP64 decision
-    float thr32 = 0.f;               // prefilter rejection threshold (> eps^2, see fp32_threshold)
+    int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tensor-core bound (+ FP64 decision)
+    float thr32 = 0.f;               // FP32 prefilter rejection threshold (> eps^2, see fp32_threshold)
     double filter_margin = 0;        // thr32 / eps^2 - 1
+    __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)), k16 = n rounded up to 16
+    float* norm16 = nullptr;         // [N] ||fp16 row||^2 (fp32)
+    int k16 = 0;                     // padded K of the MMA operands
+    double tc_scale = 1.0;           // S, a power of two
+    float thr16 = 0.f;               // tensor-core bound threshold (scaled units)
+    double margin16 = 0;             // thr16 / (S eps)^2 - 1
     uint32_t* orig = nullptr;        // [N] sorted position -> original id
     uint64_t* cell_id = nullptr;     // [G] sorted non-empty linear ids
     uint32_t* cell_start = nullptr;  // [G+1]
@@ -87,6 +94,8 @@ int varying_bits_u64(const uint64_t* keys, int64_t n, uint64_t* h_out, cudaStrea
 // Certified FP32 prefilter threshold from the per-dim spans (max - min);
 // returns 0 when the filter cannot be certified usefully.
 int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr, double* margin);
+// Certified tensor-core bound threshold (scaled units); returns 0 if not useful.
+int tc_threshold_from(double eps, int n, int K, double S, double R2, float* thr, double* margin);
 int build_index(Index* ix, const double* d_points);
 
 // ---- join (gj_join.cu) ----
@@ -114,11 +123,17 @@ struct JoinParams {
     int n, n_pad, u, sortidu, shortc;
     double eps, eps2;
     float thr32;
+    const __half* __restrict__ pts16;
+    const float* __restrict__ norm16;
+    int k16;
+    float thr16;
 };
 JoinParams join_params(const Index* ix);
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // FP32-prefilter variant (gj_join32.cu); kEmit / kCount only.
 int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+// Tensor-core bound variant (gj_join_tc.cu); kEmit / kCount only.
+int launch_join_tc(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // Number of tile positions for (rank, world, batch, n_batches); sets first/step.
 void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
                  JoinArgs* a);

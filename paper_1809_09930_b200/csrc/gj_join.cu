@@ -295,6 +295,10 @@ JoinParams join_params(const Index* ix) {
     p.eps = ix->eps;
     p.eps2 = ix->eps2;
     p.thr32 = ix->thr32;
+    p.pts16 = ix->pts16;
+    p.norm16 = ix->norm16;
+    p.k16 = ix->k16;
+    p.thr16 = ix->thr16;
     return p;
 }
 
@@ -306,7 +310,8 @@ void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank
 }
 
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
-    if (ix->fp32_filter && mode != kStats) return launch_join32(ix, mode, a, s);
+    if (ix->filter == 2 && mode != kStats) return launch_join_tc(ix, mode, a, s);
+    if (ix->filter == 1 && mode != kStats) return launch_join32(ix, mode, a, s);
     const Params p = join_params(ix);
     const int np = ix->n_pad;
     const bool sym = ix->opt.symmetric != 0;

@@ -26,7 +26,7 @@ EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_orde
 
 class Options(C.Structure):
     _fields_ = [("reorder", C.c_int32), ("sortidu", C.c_int32), ("shortc", C.c_int32), ("symmetric", C.c_int32),
-                ("sample_frac", C.c_double), ("stream", C.c_uint64), ("fp32_filter", C.c_int32),
+                ("sample_frac", C.c_double), ("stream", C.c_uint64), ("filter", C.c_int32),
                 ("reserved1", C.c_int32)]
 
 
@@ -34,7 +34,7 @@ class Info(C.Structure):
     _fields_ = [("n_points", C.c_int64), ("dim", C.c_int32), ("dim_pad", C.c_int32), ("k", C.c_int32),
                 ("u", C.c_int32), ("eps", C.c_double), ("n_cells", C.c_int64), ("n_adjacent", C.c_int64),
                 ("n_tiles", C.c_int64), ("est_candidates", C.c_double), ("build_ms", C.c_double),
-                ("fp32_filter", C.c_int32), ("filter_threshold", C.c_float), ("filter_margin", C.c_double)]
+                ("filter", C.c_int32), ("filter_threshold", C.c_float), ("filter_margin", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -95,11 +95,11 @@ def _check(rc):
 
 
 def default_options(reorder=True, sortidu=True, shortc=True, sample_frac=0.01, stream=0, symmetric=True,
-                    fp32_filter=True) -> Options:
+                    filter=2) -> Options:
     o = Options()
     lib().gj_default_options(C.byref(o))
     o.reorder, o.sortidu, o.shortc, o.symmetric = int(reorder), int(sortidu), int(shortc), int(symmetric)
-    o.fp32_filter = int(fp32_filter)
+    o.filter = int(filter)
     o.sample_frac = float(sample_frac)
     o.stream = int(stream)
     return o
@@ -127,7 +127,7 @@ class Index:
     tensor (stays on the device) or a host numpy array / tensor (staged)."""
 
     def __init__(self, points, eps: float, k: int, reorder=True, sortidu=True, shortc=True, sample_frac=0.01,
-                 stream=None, symmetric=True, fp32_filter=True):
+                 stream=None, symmetric=True, filter=2):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
@@ -139,7 +139,7 @@ class Index:
         self._keep = points
         n, dim = points.shape
         self.n_points, self.dim = int(n), int(dim)
-        self.options = default_options(reorder, sortidu, shortc, sample_frac, stream, symmetric, fp32_filter)
+        self.options = default_options(reorder, sortidu, shortc, sample_frac, stream, symmetric, filter)
         h = C.c_void_p()
         _check(lib().gj_build_index(_ptr(points), n, dim, float(eps), int(k), C.byref(self.options), C.byref(h)))
         self._h = h

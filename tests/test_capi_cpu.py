@@ -46,7 +46,7 @@ def test_library_is_built_for_sm100a(L):
 def test_host_only_entry_points(L):
     assert pkg.abi_version() == 2
     o = gpujoin.default_options()
-    assert (o.reorder, o.sortidu, o.shortc, o.symmetric, o.fp32_filter) == (1, 1, 1, 1, 1) and o.sample_frac == 0.01
+    assert (o.reorder, o.sortidu, o.shortc, o.symmetric, o.filter) == (1, 1, 1, 1, 2) and o.sample_frac == 0.01
     # computeNumBatches (§3.2.2 l.199-200)
     assert pkg.num_batches(3 * 10 ** 8, 10 ** 8) == 3
     assert pkg.num_batches(10 ** 5, 10 ** 8) == 3

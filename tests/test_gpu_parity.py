@@ -67,14 +67,14 @@ def test_pairs_equal_brute_force(gen, count, dims, eps, k):
     assert len(got) > count                       # real neighbours, not just self pairs
 
 
-@pytest.mark.parametrize("reorder,sortidu,shortc,symmetric,fp32_filter",
+@pytest.mark.parametrize("reorder,sortidu,shortc,symmetric,filt",
                          [(r, s, c, y, f) for r in (0, 1) for s in (0, 1) for c in (0, 1) for y in (0, 1)
-                          for f in (0, 1)])
-def test_every_flag_combination(reorder, sortidu, shortc, symmetric, fp32_filter):
+                          for f in (0, 1, 2)])
+def test_every_flag_combination(reorder, sortidu, shortc, symmetric, filt):
     D = synth.exponential(2200, 24, seed=5)
     got, ix = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc, symmetric=symmetric,
-                        fp32_filter=fp32_filter)
-    assert ix.info().fp32_filter == fp32_filter
+                        filter=filt)
+    assert ix.info().filter == filt
     check(D, 0.07, got)
 
 
@@ -88,27 +88,30 @@ def _near_boundary_set(eps, n, m, rel, seed):
     return np.concatenate([base, base + dirs * eps * (1 + sign * rel)])
 
 
-@pytest.mark.parametrize("rel", [1e-5, 1e-7, 3e-9])
-def test_fp32_prefilter_is_certified_near_the_boundary(rel):
-    # pairs just inside / just outside eps: the FP32 filter must never reject an
-    # inside pair, and both kernels must agree pair for pair.
+@pytest.mark.parametrize("filt", [1, 2])
+@pytest.mark.parametrize("rel", [1e-2, 1e-5, 1e-7, 3e-9])
+def test_certified_filters_near_the_boundary(rel, filt):
+    # pairs just inside / just outside eps: a certified filter must never
+    # reject an inside pair; every filter must agree with the FP64 scan pair
+    # for pair.
     eps, n = 0.05, 24
     D = _near_boundary_set(eps, n, 3000, rel, seed=int(1 / rel) % 1000)
-    a, ix32 = gpu_pairs(D, eps, 3, fp32_filter=1)
-    b, _ = gpu_pairs(D, eps, 3, fp32_filter=0)
-    assert ix32.info().fp32_filter == 1
+    a, ixf = gpu_pairs(D, eps, 3, filter=filt)
+    b, _ = gpu_pairs(D, eps, 3, filter=0)
+    assert ixf.info().filter == filt
     A = {tuple(r) for r in a.tolist()}
     assert A == {tuple(r) for r in b.tolist()}
     check(D, eps, a)
 
 
-def test_fp32_prefilter_switches_off_when_it_cannot_certify():
-    # huge coordinate spread relative to eps: the filter margin would exceed
-    # 1e-3 eps, so the index falls back to the FP64 scan (still exact).
+@pytest.mark.parametrize("filt", [1, 2])
+def test_filters_switch_off_when_they_cannot_certify(filt):
+    # huge coordinate spread relative to eps: no certified filter is useful,
+    # the index falls back to the FP64 scan (still exact).
     D = synth.uniform(1500, 8, seed=3) * 1e7
     D[:750, :] = D[:750, :] * 1e-7
-    got, ix = gpu_pairs(D, 0.05, 2, fp32_filter=1)
-    assert ix.info().fp32_filter == 0
+    got, ix = gpu_pairs(D, 0.05, 2, filter=filt)
+    assert ix.info().filter == 0
     check(D, 0.05, got)
 
 
