@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-sortidu", action="store_true")
     p.add_argument("--no-shortc", action="store_true")
     p.add_argument("--no-symmetric", action="store_true")
+    p.add_argument("--filter", type=int, default=2, choices=[0, 1, 2],
+                   help="0 FP64 scan, 1 FP32 certified prefilter, 2 tensor-core certified bound")
     p.add_argument("--batch-size", type=int, default=100_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -187,7 +189,7 @@ def main():
     stream = torch.cuda.current_stream()
     w = workload(args)
     flags = dict(reorder=not args.no_reorder, sortidu=not args.no_sortidu, shortc=not args.no_shortc,
-                 symmetric=not args.no_symmetric)
+                 symmetric=not args.no_symmetric, filter=args.filter)
 
     # ---- data: generated on rank 0's host; other ranks receive it over NCCL
     N, n = w["count"], w["dims"]
@@ -324,36 +326,47 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (k_join)
+    # ---- roofline of the dominant kernel (the join)
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
-    sm_mhz = (clk or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    fp64_peak_max = FP64_LANES_PER_SM * 2 * N_SMS * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    clk_max = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    filt = info.filter
     roof = None
     if stats is not None:
-        alg_flops = 3.0 * stats["dims_evaluated"]  # PAPER.md §4.4: 3 flops per dimension term
-        achieved = alg_flops / (jms / 1000.0) / 1e12 * (world if world > 1 else 1)
         traffic = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tfile):
-            tj = json.load(open(tfile))
-            if tj.get("workload") == args.workload:
-                traffic = tj.get("bytes_per_launch")
-        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak_max, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak_max, "traffic": traffic,
-                "kernel": "k_join (SelfJoinKernel)",
-                "peak_note": f"derived FP64: {FP64_LANES_PER_SM} FMA lanes x 2 flop x {N_SMS} SMs x max clock",
+            tj = json.load(open(tfile)).get(args.workload, {})
+            traffic = tj.get(f"filter{filt}")
+        scale = world if world > 1 else 1
+        if filt == 2:
+            # certified tensor-core bound: one n-dim dot product (2n flops) per
+            # evaluated (unordered) candidate pair, on fp16 operands
+            alg = 2.0 * n * stats["tests_evaluated"]
+            peak = peaks.get("bf16_tflops_sustained", 1389.4)
+            bound, kern = "tensor", "k_join_tc (fp16 mma.sync bound + FP64 decision)"
+            pnote = "measured cuBLAS bf16 sustained (fp16 has the same nominal dense rate)"
+        else:
+            # SHORTC scan: 3 flops per dimension evaluated (§4.4 "3n")
+            alg = 3.0 * stats["dims_evaluated"]
+            lanes = 128 if filt == 1 else FP64_LANES_PER_SM
+            peak = lanes * 2 * N_SMS * clk_max / 1e12
+            bound = "alu"
+            kern = "k_join32 (FP32 SHORTC prefilter + FP64 decision)" if filt == 1 else "k_join (FP64 SHORTC)"
+            pnote = f"derived {'FP32' if filt == 1 else 'FP64'}: {lanes} FMA lanes x 2 flop x {N_SMS} SMs x max clock"
+        achieved = alg * scale / (jms / 1000.0) / 1e12
+        roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": kern, "peak_note": pnote,
                 "alg": {"tests_evaluated": stats["tests_evaluated"], "dims_evaluated": stats["dims_evaluated"],
                         "paper_tests": stats["tests"], "paper_dims": stats["dims"], "cells": stats["cells"],
-                        "flops_per_dim": 3},
+                        "alg_tflop_per_join": alg * scale / 1e12},
                 "join_ms": jms, "join_share_of_step": jms / ms,
-                "hbm_frac_of_measured": None}
-        if peaks.get("hbm_gbs"):
-            # bytes the join must at least move: every candidate row read once per tile + pairs written
-            roof["candidate_gbs"] = stats["tests_evaluated"] * 8.0 * n / 128.0 / (jms / 1000.0) / 1e9
+                "filter_margin": info.filter_margin}
     line = {
         "metric": "self-join result pairs/s", "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": {2: "f16 MMA (f32 acc) bound + f64 decision", 1: "f32 bound + f64 decision", 0: "f64"}[filt],
+        "data": "synthetic",
         "config": {"workload": args.workload, "generator": w["gen"], "count": N, "dims": n, "eps": w["eps"],
                    "k": w["k"], **flags, "batch_size": args.batch_size, "n_batches": nb,
                    "parallelism": f"entity-partitioned dp{world}",
