@@ -64,9 +64,11 @@ typedef struct {
                             decided by the FP64 test, so the pair set is the same for all:
                             0 = FP64 SHORTC scan (Alg. 1 verbatim arithmetic)
                             1 = certified FP32 SHORTC prefilter (SIMT, packed f32x2)
-                            2 = certified tensor-core bound (fp16 MMA, fp32 accumulate) on
-                                dense cell-pair blocks (default); falls back to 1, then 0,
-                                when the data's spread makes the bound uncertifiable.
+                            2 = certified tensor-core bound on dense cell-pair blocks with
+                                tcgen05.mma (fp16 operands, fp32 accumulators in TMEM) (default)
+                            3 = the same bound with legacy mma.sync (baseline)
+                            2 and 3 fall back to 1, then 0, when the data's spread makes the
+                            bound uncertifiable.
                             gj_join_stats always runs the FP64 scan.                          */
     int32_t reserved1;
 } gj_options;
@@ -84,7 +86,7 @@ typedef struct {
     int64_t n_tiles;      /* query tiles (<= 128 queries of one cell each)         */
     double est_candidates;/* sum over queries of candidates before SORTIDU         */
     double build_ms;      /* device time of gj_build_index (CUDA events)           */
-    int32_t filter;       /* filter the join kernel actually runs (0/1/2, see gj_options) */
+    int32_t filter;       /* filter the join kernel actually runs (0..3, see gj_options) */
     float filter_threshold;  /* its rejection threshold (filter 2: in scaled units)      */
     double filter_margin; /* threshold / eps^2 - 1 (relative slack of the bound)          */
 } gj_info;
@@ -136,6 +138,11 @@ GJ_API int gj_estimate(gj_index* idx, double frac, int32_t rank, int32_t world, 
  * eps (1 + 1e-9).  *margin = thr / eps^2 - 1 (from the exact double value).
  * Returns 1 if the filter is enabled for such data, 0 if not, <0 on error. */
 GJ_API int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, double* margin);
+
+/* Diagnostic: D[128][128] = A[128][32] . B[128][32]^T (fp16 row-major device
+ * inputs, fp32 row-major device output) through the join kernel's tcgen05 /
+ * TMEM path (shared-memory layout, descriptors, TMEM load).  Synchronous. */
+GJ_API int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t stream);
 
 /* computeNumBatches (§3.2.2 l.199-200): n_b = max(3, ceil(est / batch_size)). */
 GJ_API int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size);

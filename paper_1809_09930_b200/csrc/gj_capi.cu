@@ -131,7 +131,7 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     ix.eps2 = eps * eps;
     ix.opt = o;
     ix.stream = (cudaStream_t)o.stream;
-    if (o.filter < 0 || o.filter > 2) { set_error("filter must be 0, 1 or 2"); delete h; return GJ_ERR_INVALID; }
+    if (o.filter < 0 || o.filter > 3) { set_error("filter must be 0, 1, 2 or 3"); delete h; return GJ_ERR_INVALID; }
     ix.filter = o.filter;
     const double* dX = points;
     double* staged = nullptr;
@@ -172,8 +172,8 @@ int gj_index_info(const gj_index* h, gj_info* info) {
     info->est_candidates = ix.est_candidates;
     info->build_ms = ix.build_ms;
     info->filter = ix.filter;
-    info->filter_threshold = ix.filter == 2 ? ix.thr16 : ix.thr32;
-    info->filter_margin = ix.filter == 2 ? ix.margin16 : ix.filter_margin;
+    info->filter_threshold = ix.filter >= 2 ? ix.thr16 : ix.thr32;
+    info->filter_margin = ix.filter >= 2 ? ix.margin16 : ix.filter_margin;
     return GJ_OK;
 }
 
@@ -208,6 +208,11 @@ int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, in
 int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, double* margin) {
     if (!spans || !thr || !margin || n < 1 || n > kMaxDim || !(eps > 0.0)) { set_error("bad argument"); return GJ_ERR_INVALID; }
     return fp32_threshold_from_spans(eps, n, spans, thr, margin);
+}
+
+int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t stream) {
+    if (!A || !B || !D) { set_error("null argument"); return GJ_ERR_INVALID; }
+    return selftest_umma(A, B, D, (cudaStream_t)stream);
 }
 
 int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size) {

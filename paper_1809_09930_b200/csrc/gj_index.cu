@@ -520,7 +520,7 @@ int build_index(Index* ix, const double* X) {
     if (want32) GJ_CUDA(cudaMallocAsync(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
     k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, ix->pts32); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    if (ix->filter == 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
+    if (ix->filter >= 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
         bool tc_ok = false;
         if ((rc = make_fp16(ix, &tc_ok))) return rc;
         if (!tc_ok) ix->filter = want32 ? 1 : 0;

@@ -52,7 +52,7 @@ struct Index {
     // device arrays
     double* pts = nullptr;           // [N][n_pad] reordered dims, sorted by (cell, u)
     float* pts32 = nullptr;          // [N][n_pad] fl32(x - min_j): input of the certified FP32 prefilter
-    int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tensor-core bound (+ FP64 decision)
+    int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tcgen05 bound, 3 mma.sync bound (+ FP64 decision)
     float thr32 = 0.f;               // FP32 prefilter rejection threshold (> eps^2, see fp32_threshold)
     double filter_margin = 0;        // thr32 / eps^2 - 1
     __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)), k16 = n rounded up to 16
@@ -132,8 +132,10 @@ JoinParams join_params(const Index* ix);
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // FP32-prefilter variant (gj_join32.cu); kEmit / kCount only.
 int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
-// Tensor-core bound variant (gj_join_tc.cu); kEmit / kCount only.
-int launch_join_tc(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+// Tensor-core bound variants; kEmit / kCount only.
+int launch_join_tc(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);    // mma.sync (gj_join_tc.cu)
+int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);  // tcgen05 (gj_join_umma.cu)
+int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s);
 // Number of tile positions for (rank, world, batch, n_batches); sets first/step.
 void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
                  JoinArgs* a);

@@ -310,7 +310,8 @@ void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank
 }
 
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
-    if (ix->filter == 2 && mode != kStats) return launch_join_tc(ix, mode, a, s);
+    if (ix->filter == 2 && mode != kStats) return launch_join_umma(ix, mode, a, s);
+    if (ix->filter == 3 && mode != kStats) return launch_join_tc(ix, mode, a, s);
     if (ix->filter == 1 && mode != kStats) return launch_join32(ix, mode, a, s);
     const Params p = join_params(ix);
     const int np = ix->n_pad;

@@ -116,8 +116,7 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
     const uint32_t q0 = P.tile_q0[tile];
     const uint32_t nq = min((uint32_t)kTileQ, P.cell_start[g + 1] - q0);
     const int n_pad = P.n_pad;
-    const double eps = P.eps, eps2 = P.eps2;
-    constexpr unsigned long long kMul = SYM ? 2ull : 1ull;
+    const double eps = P.eps;
 
     // A fragments (rows = this warp's queries) and per-row thresholds thr - ||q^||^2
     uint32_t af[2][KS][4];

@@ -47,6 +47,29 @@ def check(D, eps, got):
     return len(A), len(G & A)
 
 
+def test_tcgen05_selftest_gemm():
+    """The join kernel's tcgen05/TMEM path (smem descriptors, instruction
+    descriptor, TMEM lane/column mapping) on a plain 128x128x32 GEMM."""
+    from paper_1809_09930_b200 import gpujoin
+    g = torch.Generator(device="cuda").manual_seed(0)
+    A = (torch.rand(128, 32, device="cuda", generator=g) - 0.5).half()
+    B = (torch.rand(128, 32, device="cuda", generator=g) - 0.5).half()
+    D = torch.full((128, 128), float("nan"), device="cuda")
+    gpujoin.selftest_umma(A, B, D)
+    ref = A.double() @ B.double().T
+    assert torch.isfinite(D).all()
+    assert (D.double() - ref).abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("filt", [0, 1, 2, 3])
+@pytest.mark.parametrize("gen,count,dims,eps,k", [("exponential", 6000, 32, 0.08, 6), ("uniform", 3000, 16, 0.96, 6),
+                                                   ("exponential", 2500, 64, 0.16, 6), ("songs_like", 4000, 90, 0.01, 6)])
+def test_filters_on_paper_shapes(filt, gen, count, dims, eps, k):
+    D = synth.make(gen, count, dims, seed=17)
+    got, ix = gpu_pairs(D, eps, k, filter=filt)
+    check(D, eps, got)
+
+
 SMALL = [  # (generator, |D|, n, eps, k)
     ("uniform", 2000, 16, 0.96, 6),       # BASELINE configs[0] (~8 neighbours/point)
     ("exponential", 3000, 16, 0.04, 6),
@@ -69,7 +92,7 @@ def test_pairs_equal_brute_force(gen, count, dims, eps, k):
 
 @pytest.mark.parametrize("reorder,sortidu,shortc,symmetric,filt",
                          [(r, s, c, y, f) for r in (0, 1) for s in (0, 1) for c in (0, 1) for y in (0, 1)
-                          for f in (0, 1, 2)])
+                          for f in (0, 1, 2, 3)])
 def test_every_flag_combination(reorder, sortidu, shortc, symmetric, filt):
     D = synth.exponential(2200, 24, seed=5)
     got, ix = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc, symmetric=symmetric,
@@ -88,7 +111,7 @@ def _near_boundary_set(eps, n, m, rel, seed):
     return np.concatenate([base, base + dirs * eps * (1 + sign * rel)])
 
 
-@pytest.mark.parametrize("filt", [1, 2])
+@pytest.mark.parametrize("filt", [1, 2, 3])
 @pytest.mark.parametrize("rel", [1e-2, 1e-5, 1e-7, 3e-9])
 def test_certified_filters_near_the_boundary(rel, filt):
     # pairs just inside / just outside eps: a certified filter must never
@@ -104,7 +127,7 @@ def test_certified_filters_near_the_boundary(rel, filt):
     check(D, eps, a)
 
 
-@pytest.mark.parametrize("filt", [1, 2])
+@pytest.mark.parametrize("filt", [1, 2, 3])
 def test_filters_switch_off_when_they_cannot_certify(filt):
     # huge coordinate spread relative to eps: no certified filter is useful,
     # the index falls back to the FP64 scan (still exact).
