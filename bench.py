@@ -201,6 +201,24 @@ def main():
     if rank == 0:
         D_dev.copy_(torch.from_numpy(D_host))
 
+    def bcast(t):
+        """NCCL broadcast over NVLink; with --dist-backend gloo staged through host memory."""
+        if args.dist_backend == "nccl":
+            dist.broadcast(t, src=0)
+        else:
+            h = t.cpu()
+            dist.broadcast(h, src=0)
+            t.copy_(h)
+
+    def allreduce(t, op=None):
+        op = op or dist.ReduceOp.SUM
+        if args.dist_backend == "nccl":
+            dist.all_reduce(t, op=op)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+
     def barrier():
         if world > 1:
             if args.dist_backend == "nccl":
@@ -212,7 +230,7 @@ def main():
         """The timed hot path; returns (index, n_b).  ev_join brackets the join
         kernels; ev_phase (optional) = [after broadcast, after build, after estimate]."""
         if world > 1:
-            dist.broadcast(D_dev, src=0)
+            bcast(D_dev)
         if ev_phase:
             ev_phase[0].record(stream)
         ix = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
@@ -229,12 +247,12 @@ def main():
         ev_join[1].record(stream)
         if world > 1:
             tot = cnt.clone()
-            dist.all_reduce(tot)
+            allreduce(tot)
         return ix, nb
 
     # ---- capacity: exact count of this rank's share (outside any timed region)
     if world > 1:
-        dist.broadcast(D_dev, src=0)
+        bcast(D_dev)
     ix0 = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
     info = ix0.info()
     exact = ix0.estimate(1.0, rank, world)
@@ -281,9 +299,9 @@ def main():
     if world > 1:
         t = torch.tensor([ms, jms, float(pairs)], dtype=torch.float64, device=dev)
         tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        allreduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone()
-        dist.all_reduce(tsum)
+        allreduce(tsum)
         ms, jms, total_pairs = float(tmax[0]), float(tmax[1]), int(tsum[2])
     else:
         total_pairs = pairs
@@ -315,7 +333,7 @@ def main():
         e2e_t = float(np.mean(e2e_s))
         if world > 1:
             t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            allreduce(t, op=dist.ReduceOp.MAX)
             e2e_t = float(t[0])
         e2e = {"value": total_pairs / e2e_t, "unit": "pairs/s", "seconds": e2e_t,
                "h2d_bytes_per_step": int(N * n * 8), "d2h_bytes_per_step": int(pairs * 8 + 8 * 3 * 8),

@@ -172,7 +172,7 @@ int gj_index_info(const gj_index* h, gj_info* info) {
     info->est_candidates = ix.est_candidates;
     info->build_ms = ix.build_ms;
     info->filter = ix.filter;
-    info->filter_threshold = ix.filter >= 2 ? ix.thr16 : ix.thr32;
+    info->filter_threshold = ix.filter >= 2 ? (float)ix.thr16 : ix.thr32;
     info->filter_margin = ix.filter >= 2 ? ix.margin16 : ix.filter_margin;
     return GJ_OK;
 }

@@ -368,39 +368,46 @@ static bool fp32_threshold(Index* ix) {
     return fp32_threshold_from_spans(ix->eps, ix->n, spans, &ix->thr32, &ix->filter_margin) != 0;
 }
 
-// Threshold of the certified tensor-core bound (gj_join_tc.cu; DESIGN.md
-// §"Tensor-core bound").  Scaled, centred fp16 operands x^ = fp16(S (x - min)),
-// R2 = max ||x^||^2, K = padded MMA depth.  The kernel rejects a pair when
-// v = fl32(||c^||^2 - 2 acc) > fl32(thr - ||q^||^2), acc = the tensor-core fp32
-// accumulation of q^.c^.  Error terms (all conservative):
-//   delta : | ||q^ - c^|| - S||q - c|| | <= 2^-11 (||q'|| + ||c'||) + sqrt(n) 2^-24
-//   kappa : |acc - q^.c^| <= kappa R2, kappa = (K + 2) 2^-21 (4x a truncating fp32 adder)
-//   E1    : 2 kappa R2 + 4 R2 2^-24          (accumulation, v and norm roundings)
-//   E2    : 2^-23 (T0 + R2) * 1.01           (rounding of thr - ||q^||^2)
-// T = (S eps (1 + 1e-9) + delta)^2 + E1 + E2  =>  v > fl32(T - ||q^||^2) implies
-// ||q - c|| > eps (1 + 1e-9).  Enabled when the relative slack T/(S eps)^2 - 1 < 0.25.
-int tc_threshold_from(double eps, int n, int K, double S, double R2, float* thr, double* margin) {
+// Threshold of the certified tensor-core bound (gj_join_umma.cu / gj_join_tc.cu;
+// DESIGN.md §"Tensor-core bound").  Operands: x^ = fp16(S (x - min)) for the
+// n coordinates, R2 = max ||x^||^2, K = padded MMA depth (n + 4 augmented
+// columns, rounded up to 16).  A query row carries (r_hi, r_lo, 1, 1) and a
+// candidate row (1, 1, h_hi, h_lo) in the augmented columns, with
+// r = (T - ||q^||^2)/2 and h = -||c^||^2/2 split into fp16 hi + lo, so the
+// tensor core accumulates acc = q^.c^ + r + h = (T - ||q^ - c^||^2)/2 (+ err).
+//   err   <= a + b T,  a = kappa (2.001 R2) + 2^-22 R2 + 2^-23 + 2^-51 R2,
+//                      b = 0.5005 kappa + 2^-23 + 2^-51,
+//            kappa = (K + 2) 2^-21 (4x a truncating fp32 adder, products exact),
+//            2^-22 |r|, 2^-22 |h| from the hi/lo splits
+//   delta : | ||q^ - c^|| - S ||q - c|| | <= 2^-11 (||q'|| + ||c'||) + sqrt(n) 2^-24
+// A pair is rejected iff acc <= 0 (sign bit set), which implies
+// ||q^ - c^||^2 >= T - 2 err, hence S||q - c|| >= sqrt(T - 2 err) - delta, so with
+//   T = ((S eps (1 + 1e-9) + delta)^2 + 2a) / (1 - 2b)
+// every rejected pair has ||q - c|| >= eps (1 + 1e-9).  Enabled when the
+// relative slack T / (S eps)^2 - 1 < 0.25.
+int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr, double* margin) {
+    const double u11 = std::ldexp(1.0, -11);
     const double R = std::sqrt(R2);
-    const double Rp = (R + std::sqrt((double)n) * std::ldexp(1.0, -25)) / (1.0 - std::ldexp(1.0, -11));
-    const double delta = std::ldexp(1.0, -11) * 2.0 * Rp + std::sqrt((double)n) * std::ldexp(1.0, -24);
+    const double Rp = (R + std::sqrt((double)n) * std::ldexp(1.0, -25)) / (1.0 - u11);
+    const double delta = u11 * 2.0 * Rp + std::sqrt((double)n) * std::ldexp(1.0, -24);
     const double kappa = (K + 2) * std::ldexp(1.0, -21);
-    const double E1 = 2.0 * kappa * R2 + 4.0 * R2 * std::ldexp(1.0, -24);
+    const double a = kappa * 2.001 * R2 + std::ldexp(1.0, -22) * R2 + std::ldexp(1.0, -23) + std::ldexp(1.0, -51) * R2;
+    const double b = 0.5005 * kappa + std::ldexp(1.0, -23) + std::ldexp(1.0, -51);
     const double epsS = S * eps * (1.0 + 1e-9);
-    const double T0 = (epsS + delta) * (epsS + delta) + E1;
-    const double E2 = std::ldexp(1.0, -23) * (T0 + R2) * 1.01;
-    const double T = T0 + E2;
-    float T32 = (float)T;
-    if ((double)T32 < T) T32 = std::nextafter(T32, INFINITY);
-    *thr = T32;
+    const double T = ((epsS + delta) * (epsS + delta) + 2.0 * a) / (1.0 - 2.0 * b) * (1.0 + 1e-12);
+    *thr = T;
     *margin = T / ((S * eps) * (S * eps)) - 1.0;
-    return std::isfinite(T) && T32 < 1e30f && *margin < 0.25;
+    // fp16 range: r, h, R2 and the padding sentinel must stay well inside 65504
+    return std::isfinite(T) && *margin < 0.25 && T < 40000.0 && R2 < 40000.0;
 }
 
 namespace {
+constexpr float kSentinel = -65504.f;   // most negative finite fp16: forces acc < 0
+
 // pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond; norm16[p] =
-// ||pts16[p]||^2 (fp64 sum, rounded to fp32); R2 = max over p (exact doubles).
+// ||x^_p||^2 exactly (fp64); R2 = max over p.
 __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, int k16, double S,
-                         const Meta* __restrict__ meta, __half* __restrict__ pts16, float* __restrict__ norm16,
+                         const Meta* __restrict__ meta, __half* __restrict__ pts16, double* __restrict__ norm16,
                          unsigned long long* __restrict__ r2max) {
     __shared__ double mn[kMaxDim];
     for (int t = threadIdx.x; t < n; t += blockDim.x) mn[t] = meta->mins[meta->order[t]];
@@ -415,35 +422,53 @@ __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n
             const double hd = (double)__half2float(h);
             nrm += hd * hd;
         }
-        norm16[p] = (float)nrm;
+        norm16[p] = nrm;
     }
-    // block max of the (non-negative) norms via their ordered bit patterns
     unsigned long long bits = (unsigned long long)__double_as_longlong(nrm);
 #pragma unroll
     for (int o = 16; o; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
     if ((threadIdx.x & 31) == 0) atomicMax(r2max, bits);
 }
+
+// Candidate-side augmented columns: (1, 1, h_hi, h_lo), h = -||x^||^2 / 2.
+__global__ void k_aug16(int64_t N, int k16, const double* __restrict__ norm16, __half* __restrict__ pts16) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const double h = -0.5 * norm16[p];
+    const __half hh = __double2half(h);
+    const __half hl = __double2half(h - (double)__half2float(hh));
+    __half* row = pts16 + p * k16 + (k16 - 4);
+    row[0] = __float2half(1.f);
+    row[1] = __float2half(1.f);
+    row[2] = hh;
+    row[3] = hl;
+}
 }  // namespace
 
-// Builds the fp16 operands; returns true if the tensor-core bound is certified.
+// Builds the fp16 operands; *ok = true if the tensor-core bound is certified.
 static int make_fp16(Index* ix, bool* ok) {
     cudaStream_t s = ix->stream;
     const Meta& m = ix->h_meta;
-    double smax = 0.0;
-    for (int t = 0; t < ix->n; ++t) smax = std::max(smax, m.maxs[m.order[t]] - m.mins[m.order[t]]);
+    double ss = 0.0;
+    for (int t = 0; t < ix->n; ++t) {
+        const double sj = m.maxs[m.order[t]] - m.mins[m.order[t]];
+        ss += sj * sj;
+    }
     *ok = false;
-    if (!(smax < 1e300)) return GJ_OK;
-    // S: power of two putting the largest centred coordinate in [2^13, 2^14)
-    ix->tc_scale = smax > 0.0 ? std::ldexp(1.0, (int)std::floor(std::log2(16384.0 / smax))) : 1.0;
-    ix->k16 = (ix->n + 15) & ~15;
+    const double span = std::max(std::sqrt(ss), ix->eps);   // >= every ||x - min|| and eps
+    if (!(span < 1e300) || !(span > 0.0)) return GJ_OK;
+    // S: power of two with S * span in [90, 180]: r, h, R2 and the sentinel fit fp16
+    ix->tc_scale = std::ldexp(1.0, (int)std::floor(std::log2(180.0 / span)));
+    ix->k16 = (ix->n + 4 + 15) & ~15;
     const int64_t N = ix->N;
     GJ_CUDA(cudaMallocAsync(&ix->pts16, (size_t)N * ix->k16 * sizeof(__half), s));
-    GJ_CUDA(cudaMallocAsync(&ix->norm16, (size_t)N * sizeof(float), s));
+    GJ_CUDA(cudaMallocAsync(&ix->norm16, (size_t)N * sizeof(double), s));
     unsigned long long* d_r2 = nullptr;
     GJ_CUDA(cudaMallocAsync(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
     k_make16<<<blocks_for(N, 256), 256, 0, s>>>(ix->pts, N, ix->n, ix->n_pad, ix->k16, ix->tc_scale, ix->meta,
                                                  ix->pts16, ix->norm16, d_r2); count_launch();
+    k_aug16<<<blocks_for(N, 256), 256, 0, s>>>(N, ix->k16, ix->norm16, ix->pts16); count_launch();
     GJ_CUDA(cudaGetLastError());
     unsigned long long h_r2 = 0;
     GJ_CUDA(cudaMemcpyAsync(&h_r2, d_r2, sizeof(h_r2), cudaMemcpyDeviceToHost, s));

@@ -55,11 +55,11 @@ struct Index {
     int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tcgen05 bound, 3 mma.sync bound (+ FP64 decision)
     float thr32 = 0.f;               // FP32 prefilter rejection threshold (> eps^2, see fp32_threshold)
     double filter_margin = 0;        // thr32 / eps^2 - 1
-    __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)), k16 = n rounded up to 16
-    float* norm16 = nullptr;         // [N] ||fp16 row||^2 (fp32)
-    int k16 = 0;                     // padded K of the MMA operands
+    __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)) + candidate-side augmented columns
+    double* norm16 = nullptr;        // [N] ||fp16 coordinates||^2 (exact, fp64)
+    int k16 = 0;                     // MMA depth: n + 4 augmented columns, rounded up to 16
     double tc_scale = 1.0;           // S, a power of two
-    float thr16 = 0.f;               // tensor-core bound threshold (scaled units)
+    double thr16 = 0.0;              // tensor-core bound threshold T (scaled units)
     double margin16 = 0;             // thr16 / (S eps)^2 - 1
     uint32_t* orig = nullptr;        // [N] sorted position -> original id
     uint64_t* cell_id = nullptr;     // [G] sorted non-empty linear ids
@@ -95,7 +95,7 @@ int varying_bits_u64(const uint64_t* keys, int64_t n, uint64_t* h_out, cudaStrea
 // returns 0 when the filter cannot be certified usefully.
 int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr, double* margin);
 // Certified tensor-core bound threshold (scaled units); returns 0 if not useful.
-int tc_threshold_from(double eps, int n, int K, double S, double R2, float* thr, double* margin);
+int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr, double* margin);
 int build_index(Index* ix, const double* d_points);
 
 // ---- join (gj_join.cu) ----
@@ -124,11 +124,25 @@ struct JoinParams {
     double eps, eps2;
     float thr32;
     const __half* __restrict__ pts16;
-    const float* __restrict__ norm16;
+    const double* __restrict__ norm16;
     int k16;
-    float thr16;
+    double thr16;
 };
 JoinParams join_params(const Index* ix);
+
+// Query-side augmented MMA columns (r_hi, r_lo) of the tensor-core bound:
+// r = (T - ||q^||^2) / 2 split into fp16 hi + lo; invalid rows get the
+// sentinel -65504 so that every accumulator of the row is negative.
+__device__ __forceinline__ void query_aug(double T, double nq, bool valid, __half& rhi, __half& rlo) {
+    if (!valid) {
+        rhi = __float2half(-65504.f);
+        rlo = __float2half(0.f);
+        return;
+    }
+    const double r = 0.5 * (T - nq);
+    rhi = __double2half(r);
+    rlo = __double2half(r - (double)__half2float(rhi));
+}
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // FP32-prefilter variant (gj_join32.cu); kEmit / kCount only.
 int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);

@@ -35,9 +35,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -102,7 +99,6 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
     constexpr int RS = KP + 8;         // smem row stride in halves (16 B pad: conflict-free ldmatrix)
     constexpr int CH = KP / 8;         // 16-byte chunks per candidate row
     __shared__ __align__(16) __half Bs[2][kBN * RS];
-    __shared__ __align__(16) float Cn[2][kBN];
     __shared__ uint32_t s_win[2];
     __shared__ unsigned long long s_red[kTileQ / 32];
 
@@ -118,9 +114,10 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
-    // A fragments (rows = this warp's queries) and per-row thresholds thr - ||q^||^2
+    // A fragments (rows = this warp's queries); the augmented columns K-4..K-1
+    // (lane tq = 2: r_hi, r_lo; tq = 3: 1, 1) turn every accumulator into
+    // (T - ||q^ - c^||^2) / 2 (see tc_threshold_from)
     uint32_t af[2][KS][4];
-    float thr_r[2][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
@@ -128,12 +125,22 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
             const int row = 32 * warp + 16 * mt + gq + 8 * h;
             const bool valid = row < (int)nq;
             const uint32_t prow = q0 + (valid ? row : 0);
-            thr_r[mt][h] = valid ? P.thr16 - P.norm16[prow] : -INFINITY;
             const __half* src = P.pts16 + (size_t)prow * KP + 2 * tq;
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 af[mt][ks][h] = *reinterpret_cast<const uint32_t*>(src + 16 * ks);
                 af[mt][ks][2 + h] = *reinterpret_cast<const uint32_t*>(src + 16 * ks + 8);
+            }
+            if (tq >= 2) {
+                __half2 aug;
+                if (tq == 2) {
+                    __half rhi, rlo;
+                    query_aug(P.thr16, P.norm16[prow], valid, rhi, rlo);
+                    aug = __halves2half2(rhi, rlo);
+                } else {
+                    aug = __halves2half2(__float2half(1.f), __float2half(1.f));
+                }
+                af[mt][KS - 1][2 + h] = *reinterpret_cast<uint32_t*>(&aug);
             }
         }
     }
@@ -193,12 +200,14 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
             for (int i = tid; i < kBN * CH; i += kTileQ) {
                 const int row = i / CH, ch = i - row * CH;
                 __half* dst = &Bs[buf][row * RS + ch * 8];
-                if (row < cnt) cp_async16(dst, P.pts16 + (size_t)(start + row) * KP + ch * 8);
-                else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-            }
-            for (int i = tid; i < kBN; i += kTileQ) {
-                if (i < cnt) cp_async4(&Cn[buf][i], P.norm16 + start + i);
-                else Cn[buf][i] = INFINITY;   // padding candidates are always rejected
+                if (row < cnt) {
+                    cp_async16(dst, P.pts16 + (size_t)(start + row) * KP + ch * 8);
+                } else {   // padding candidate: zeros, h_hi = -65504 -> every accumulator < 0
+                    union { uint4 u; __half h[8]; } c;
+                    c.u = make_uint4(0, 0, 0, 0);
+                    if (ch == CH - 1) c.h[6] = __float2half(-65504.f);
+                    *reinterpret_cast<uint4*>(dst) = c.u;
+                }
             }
             cp_async_commit();
         };
@@ -243,34 +252,23 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
 #pragma unroll
                     for (int ks = 0; ks < KS; ++ks) mma16816(acc[mt][nt], af[mt][ks], bf[ks][0], bf[ks][1]);
             }
-            // epilogue: v = ||c^||^2 - 2 acc; survivor iff v <= thr - ||q^||^2
-            const float* cn = Cn[buf];
-            bool any = false;
+            // epilogue: acc = (T - ||q^ - c^||^2) / 2 + err; survivor iff acc > +0
+            uint32_t all = 0xffffffffu;
 #pragma unroll
-            for (int nt = 0; nt < 8; ++nt) {
-                const float2 c2 = *reinterpret_cast<const float2*>(cn + 8 * nt + 2 * tq);
+            for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    any |= fmaf(-2.f, acc[mt][nt][0], c2.x) <= thr_r[mt][0];
-                    any |= fmaf(-2.f, acc[mt][nt][1], c2.y) <= thr_r[mt][0];
-                    any |= fmaf(-2.f, acc[mt][nt][2], c2.x) <= thr_r[mt][1];
-                    any |= fmaf(-2.f, acc[mt][nt][3], c2.y) <= thr_r[mt][1];
-                }
-            }
-            if (any) {   // rare: decide the survivors in FP64
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) all &= __float_as_uint(acc[mt][nt][e]);
+            if (!(all >> 31)) {   // rare: decide the survivors in FP64
                 unsigned long long mask = 0;
 #pragma unroll
-                for (int nt = 0; nt < 8; ++nt) {
-                    const float2 c2 = *reinterpret_cast<const float2*>(cn + 8 * nt + 2 * tq);
+                for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-                    for (int mt = 0; mt < 2; ++mt) {
+                    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float v = fmaf(-2.f, acc[mt][nt][e], (e & 1) ? c2.y : c2.x);
-                            if (v <= thr_r[mt][e >> 1]) mask |= 1ull << (nt * 8 + mt * 4 + e);
-                        }
-                    }
-                }
+                        for (int e = 0; e < 4; ++e)
+                            if (!(__float_as_uint(acc[mt][nt][e]) >> 31)) mask |= 1ull << (nt * 8 + mt * 4 + e);
                 while (mask) {
                     const int bit = __ffsll((long long)mask) - 1;
                     mask &= mask - 1;

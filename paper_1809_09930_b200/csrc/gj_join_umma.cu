@@ -63,7 +63,6 @@ template <int KP>
 struct Smem {
     alignas(128) __half a[kM * KP];
     alignas(128) __half b[kBufs][kN * KP];
-    alignas(16) float cn[kBufs][kN];
     uint64_t mbar[2];
     uint32_t tmem_base;
     uint32_t win[2];
@@ -97,18 +96,27 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
         umma::mbar_fence_init();
     }
     const uint32_t a_s = umma::smem_u32(S.a);
+    unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a);
     for (int i = tid; i < kM * (KP / 8); i += kThreads) {
         const int row = i / (KP / 8), kc = i % (KP / 8);
-        const uint32_t dst = a_s + umma::tile_off(row, kc * 8, KP);
-        if (row < (int)nq) umma::cp_async16(dst, P.pts16 + (size_t)(q0 + row) * KP + kc * 8);
-        else *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(S.a) + (dst - a_s)) = make_uint4(0, 0, 0, 0);
+        const uint32_t off = umma::tile_off(row, kc * 8, KP);
+        const bool valid = row < (int)nq;
+        if (kc < KP / 8 - 1) {
+            if (valid) umma::cp_async16(a_s + off, P.pts16 + (size_t)(q0 + row) * KP + kc * 8);
+            else *reinterpret_cast<uint4*>(a_raw + off) = make_uint4(0, 0, 0, 0);
+        } else {   // last chunk: coordinates (if any) + query-side augmented columns (r_hi, r_lo, 1, 1)
+            union { uint4 u; __half h[8]; } c;
+            c.u = valid ? *reinterpret_cast<const uint4*>(P.pts16 + (size_t)(q0 + row) * KP + kc * 8) : make_uint4(0, 0, 0, 0);
+            query_aug(P.thr16, valid ? P.norm16[q0 + row] : 0.0, valid, c.h[4], c.h[5]);
+            c.h[6] = __float2half(1.f);
+            c.h[7] = __float2half(1.f);
+            *reinterpret_cast<uint4*>(a_raw + off) = c.u;
+        }
     }
     umma::cp_async_commit();
     // this thread's epilogue row (TMEM lane) and column half
     const int erow = 32 * (warp & 3) + lane;
     const int ecol0 = 64 * (warp >> 2);
-    const bool rvalid = erow < (int)nq;
-    const float thr_row = rvalid ? P.thr16 - P.norm16[q0 + erow] : -INFINITY;
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
@@ -173,12 +181,14 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
             for (int i = tid; i < kN * (KP / 8); i += kThreads) {
                 const int row = i / (KP / 8), kc = i % (KP / 8);
                 const uint32_t off = umma::tile_off(row, kc * 8, KP);
-                if (row < cnt) umma::cp_async16(b_s + off, P.pts16 + (size_t)(start + row) * KP + kc * 8);
-                else *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(S.b[buf]) + off) = make_uint4(0, 0, 0, 0);
-            }
-            for (int i = tid; i < kN; i += kThreads) {
-                if (i < cnt) umma::cp_async4(umma::smem_u32(&S.cn[buf][i]), P.norm16 + start + i);
-                else S.cn[buf][i] = INFINITY;   // padding candidates are always rejected
+                if (row < cnt) {
+                    umma::cp_async16(b_s + off, P.pts16 + (size_t)(start + row) * KP + kc * 8);
+                } else {   // padding candidate: zeros, h_hi = -65504 -> every accumulator < 0
+                    union { uint4 u; __half h[8]; } c;
+                    c.u = make_uint4(0, 0, 0, 0);
+                    if (kc == KP / 8 - 1) c.h[6] = __float2half(-65504.f);
+                    *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(S.b[buf]) + off) = c.u;
+                }
             }
         };
         auto epilogue = [&](int kb) {
@@ -187,20 +197,23 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
             phase[ab] ^= 1u;
             umma::fence_after();
             const uint32_t cbase = r + (uint32_t)kb * kN;
-            const float* cn = S.cn[kb % kBufs];
+            // acc = (T - ||q^ - c^||^2) / 2 + err: a pair survives iff acc > +0 (sign bit clear)
+            float v[2][32];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                umma::tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(ab * kN + ecol0 + 32 * h), v[h]);
+            uint32_t all = 0xffffffffu;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) all &= __float_as_uint(v[h][i]);
             unsigned long long mask = 0;
+            if (!(all >> 31)) {   // rare: some accumulator non-negative
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float v[32];
-                umma::tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(ab * kN + ecol0 + 32 * h), v);
+                for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    const float4 c4 = *reinterpret_cast<const float4*>(cn + ecol0 + 32 * h + i);
-                    if (fmaf(-2.f, v[i], c4.x) <= thr_row) mask |= 1ull << (32 * h + i);
-                    if (fmaf(-2.f, v[i + 1], c4.y) <= thr_row) mask |= 1ull << (32 * h + i + 1);
-                    if (fmaf(-2.f, v[i + 2], c4.z) <= thr_row) mask |= 1ull << (32 * h + i + 2);
-                    if (fmaf(-2.f, v[i + 3], c4.w) <= thr_row) mask |= 1ull << (32 * h + i + 3);
-                }
+                    for (int i = 0; i < 32; ++i)
+                        if (!(__float_as_uint(v[h][i]) >> 31)) mask |= 1ull << (32 * h + i);
             }
             umma::fence_before();
             while (mask) {   // rare: FP64 decision of the survivors
