@@ -139,6 +139,13 @@ GJ_API int gj_estimate(gj_index* idx, double frac, int32_t rank, int32_t world, 
  * Returns 1 if the filter is enabled for such data, 0 if not, <0 on error. */
 GJ_API int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, double* margin);
 
+/* Host only: threshold T of the certified tensor-core bound (filter 2/3) for
+ * radius eps, n coordinates, MMA depth K (>= n + 4), power-of-two scale S and
+ * R2 = max squared norm of the fp16 operand rows.  The kernel rejects a pair
+ * iff its accumulator q^.c^ + (T - ||q^||^2)/2 - ||c^||^2/2 is <= 0, which
+ * implies dist > eps (1 + 1e-9).  Returns 1 if usable, 0 if not, <0 on error. */
+GJ_API int gj_tc_threshold(double eps, int32_t n, int32_t K, double S, double R2, double* thr, double* margin);
+
 /* Diagnostic: D[128][128] = A[128][32] . B[128][32]^T (fp16 row-major device
  * inputs, fp32 row-major device output) through the join kernel's tcgen05 /
  * TMEM path (shared-memory layout, descriptors, TMEM load).  Synchronous. */

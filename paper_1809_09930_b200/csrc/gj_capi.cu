@@ -210,6 +210,14 @@ int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, do
     return fp32_threshold_from_spans(eps, n, spans, thr, margin);
 }
 
+int gj_tc_threshold(double eps, int32_t n, int32_t K, double S, double R2, double* thr, double* margin) {
+    if (!thr || !margin || n < 1 || K < n + 4 || !(eps > 0.0) || !(S > 0.0) || !(R2 >= 0.0)) {
+        set_error("bad argument");
+        return GJ_ERR_INVALID;
+    }
+    return tc_threshold_from(eps, n, K, S, R2, thr, margin);
+}
+
 int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t stream) {
     if (!A || !B || !D) { set_error("null argument"); return GJ_ERR_INVALID; }
     return selftest_umma(A, B, D, (cudaStream_t)stream);

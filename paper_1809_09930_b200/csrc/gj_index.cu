@@ -402,46 +402,43 @@ int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr
 }
 
 namespace {
-constexpr float kSentinel = -65504.f;   // most negative finite fp16: forces acc < 0
-
-// pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond; norm16[p] =
-// ||x^_p||^2 exactly (fp64); R2 = max over p.
+// pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond (one thread per element).
 __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, int k16, double S,
-                         const Meta* __restrict__ meta, __half* __restrict__ pts16, double* __restrict__ norm16,
-                         unsigned long long* __restrict__ r2max) {
+                         const Meta* __restrict__ meta, __half* __restrict__ pts16) {
     __shared__ double mn[kMaxDim];
     for (int t = threadIdx.x; t < n; t += blockDim.x) mn[t] = meta->mins[meta->order[t]];
     __syncthreads();
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * k16) return;
+    const int64_t p = e / k16;
+    const int t = (int)(e - p * k16);
+    pts16[e] = t < n ? __double2half(S * (pts[p * n_pad + t] - mn[t])) : __float2half(0.f);
+}
+
+// norm16[p] = ||x^_p||^2 exactly (fp64), R2 = max over p, and the candidate-side
+// augmented columns (1, 1, h_hi, h_lo), h = -||x^_p||^2 / 2 (one thread per point).
+__global__ void k_norm16(int64_t N, int n, int k16, __half* __restrict__ pts16, double* __restrict__ norm16,
+                         unsigned long long* __restrict__ r2max) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double nrm = 0.0;
     if (p < N) {
-        for (int t = 0; t < k16; ++t) {
-            __half h = __float2half(0.f);
-            if (t < n) h = __double2half(S * (pts[p * n_pad + t] - mn[t]));
-            pts16[p * k16 + t] = h;
-            const double hd = (double)__half2float(h);
+        __half* row = pts16 + p * k16;
+        for (int t = 0; t < n; ++t) {
+            const double hd = (double)__half2float(row[t]);
             nrm += hd * hd;
         }
         norm16[p] = nrm;
+        const double h = -0.5 * nrm;
+        const __half hh = __double2half(h);
+        row[k16 - 4] = __float2half(1.f);
+        row[k16 - 3] = __float2half(1.f);
+        row[k16 - 2] = hh;
+        row[k16 - 1] = __double2half(h - (double)__half2float(hh));
     }
     unsigned long long bits = (unsigned long long)__double_as_longlong(nrm);
 #pragma unroll
     for (int o = 16; o; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
     if ((threadIdx.x & 31) == 0) atomicMax(r2max, bits);
-}
-
-// Candidate-side augmented columns: (1, 1, h_hi, h_lo), h = -||x^||^2 / 2.
-__global__ void k_aug16(int64_t N, int k16, const double* __restrict__ norm16, __half* __restrict__ pts16) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    const double h = -0.5 * norm16[p];
-    const __half hh = __double2half(h);
-    const __half hl = __double2half(h - (double)__half2float(hh));
-    __half* row = pts16 + p * k16 + (k16 - 4);
-    row[0] = __float2half(1.f);
-    row[1] = __float2half(1.f);
-    row[2] = hh;
-    row[3] = hl;
 }
 }  // namespace
 
@@ -466,9 +463,9 @@ static int make_fp16(Index* ix, bool* ok) {
     unsigned long long* d_r2 = nullptr;
     GJ_CUDA(cudaMallocAsync(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
-    k_make16<<<blocks_for(N, 256), 256, 0, s>>>(ix->pts, N, ix->n, ix->n_pad, ix->k16, ix->tc_scale, ix->meta,
-                                                 ix->pts16, ix->norm16, d_r2); count_launch();
-    k_aug16<<<blocks_for(N, 256), 256, 0, s>>>(N, ix->k16, ix->norm16, ix->pts16); count_launch();
+    k_make16<<<blocks_for(N * ix->k16, 256), 256, 0, s>>>(ix->pts, N, ix->n, ix->n_pad, ix->k16, ix->tc_scale,
+                                                          ix->meta, ix->pts16); count_launch();
+    k_norm16<<<blocks_for(N, 256), 256, 0, s>>>(N, ix->n, ix->k16, ix->pts16, ix->norm16, d_r2); count_launch();
     GJ_CUDA(cudaGetLastError());
     unsigned long long h_r2 = 0;
     GJ_CUDA(cudaMemcpyAsync(&h_r2, d_r2, sizeof(h_r2), cudaMemcpyDeviceToHost, s));

@@ -22,7 +22,12 @@ namespace {
 constexpr int kM = 128;         // queries per tile (UMMA M)
 constexpr int kN = 128;         // candidates per block (UMMA N)
 constexpr int kThreads = 256;   // 8 warps
-constexpr int kBufs = 3;        // B ring
+// B ring depth: as many 128-candidate stages as fit next to the A tile in
+// ~100 KB (two CTAs per SM), at least 3; prefetch distance = stages - 1.
+template <int KP>
+constexpr int stages() {
+    return (100 * 1024 - kM * KP * 2) / (kN * KP * 2) < 3 ? 3 : ((100 * 1024 - kM * KP * 2) / (kN * KP * 2) > 8 ? 8 : (100 * 1024 - kM * KP * 2) / (kN * KP * 2));
+}
 
 __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const double* __restrict__ b,
                                              int n_pad) {
@@ -62,7 +67,7 @@ __device__ __noinline__ unsigned long long decide_and_emit(const JoinParams& P, 
 template <int KP>
 struct Smem {
     alignas(128) __half a[kM * KP];
-    alignas(128) __half b[kBufs][kN * KP];
+    alignas(128) __half b[stages<KP>()][kN * KP];
     uint64_t mbar[2];
     uint32_t tmem_base;
     uint32_t win[2];
@@ -74,6 +79,7 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem<KP>& S = *reinterpret_cast<Smem<KP>*>(smem_raw);
     constexpr int KS = KP / 16;
+    constexpr int kBufs = stages<KP>();
     constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, kN);
     constexpr uint32_t kSBO = KP * 16;   // bytes between 8-row groups
 
@@ -225,12 +231,13 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
             }
         };
 
-        load_block(0);
-        umma::cp_async_commit();
-        if (nblk > 1) load_block(1);
-        umma::cp_async_commit();
+#pragma unroll
+        for (int p = 0; p < kBufs - 1; ++p) {   // prologue: prefetch kBufs-1 blocks
+            if (p < nblk) load_block(p);
+            umma::cp_async_commit();
+        }
         for (int kb = 0; kb < nblk; ++kb) {
-            umma::cp_async_wait<1>();   // block kb (and the A tile) landed; kb+1 may be in flight
+            umma::cp_async_wait<kBufs - 2>();   // block kb (and the A tile) landed; later ones may be in flight
             umma::fence_proxy_async();
             __syncthreads();
             if (tid == 0) {
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
                 umma::commit(&S.mbar[kb & 1]);
             }
             if (kb >= 1) epilogue(kb - 1);   // overlaps MMA(kb)
-            if (kb + 2 < nblk) load_block(kb + 2);   // buffer of block kb-1, whose MMA has completed
+            if (kb + kBufs - 1 < nblk) load_block(kb + kBufs - 1);   // buffer of block kb-1 (its MMA completed)
             umma::cp_async_commit();
         }
         epilogue(nblk - 1);
@@ -322,6 +329,7 @@ int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym,
     // request enough dynamic smem that at most 2 CTAs share an SM: the two
     // CTAs' 2 x 256 TMEM columns fill the SM's 512
     const size_t smem = std::max<size_t>(sizeof(Smem<KP>), 80 * 1024);
+    static_assert(sizeof(Smem<KP>) <= 227 * 1024, "shared memory");
     static bool attr_done[2][2] = {{false, false}, {false, false}};
     auto setattr = [&](const void* f, int m, int y) -> int {
         if (!attr_done[m][y]) {

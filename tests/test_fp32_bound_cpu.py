@@ -73,3 +73,39 @@ def test_threshold_margin_and_switch_off():
     assert on and 0 < margin < 1e-4 and float(thr) >= 0.08 ** 2
     off, _, _ = gpujoin.fp32_threshold(1e-6, np.full(32, 1e3))     # A > 1e-3 eps -> disabled
     assert not off
+
+
+@pytest.mark.parametrize("n,eps,span", [(16, 0.05, 1.0), (16, 0.55, 1.0), (32, 0.08, 0.5), (64, 0.16, 1.0),
+                                        (90, 0.01, 1.0)])
+def test_tensor_core_bound_keeps_inside_pairs(n, eps, span):
+    """gj_tc_threshold: for pairs whose exact distance is at/just inside eps,
+    exact rounding of the operands to fp16 (as k_make16 does) leaves
+    (T - ||q^ - c^||^2) / 2 above the documented worst-case accumulation
+    error, so such a pair can never be rejected by the sign test."""
+    rng = np.random.default_rng(n)
+    S = 2.0 ** np.floor(np.log2(180.0 / max(np.sqrt(n) * span, eps)))
+    K = (n + 4 + 15) // 16 * 16
+    worst = None
+    pairs = []
+    for _ in range(200):
+        q = rng.random(n) * span
+        v = rng.standard_normal(n)
+        v /= np.linalg.norm(v)
+        c = np.clip(q + v * eps * (1 - rng.random() * 1e-7), 0, span)
+        if np.sum((q - c) ** 2) <= eps * eps:
+            pairs.append((q, c))
+    qh = [np.float16(S * q).astype(np.float64) for q, _ in pairs]
+    ch = [np.float16(S * c).astype(np.float64) for _, c in pairs]
+    R2 = max(max(np.dot(a, a) for a in qh), max(np.dot(b, b) for b in ch))
+    ok, T, margin = gpujoin.tc_threshold(eps, n, K, S, R2)
+    assert margin > 0
+    if not ok:   # the index would fall back to the FP32 / FP64 scan
+        assert margin >= 0.25
+        pytest.skip("bound not certifiable for this spread")
+    kappa = (K + 2) * 2.0 ** -21
+    err = kappa * (2.001 * R2 + 0.5005 * T) + 2.0 ** -22 * (T / 2 + R2) + 2.0 ** -23
+    for a, b in zip(qh, ch):
+        d2 = sum((Fraction(float(x)) - Fraction(float(y))) ** 2 for x, y in zip(a, b))
+        slack = (Fraction(T) - d2) / 2 - Fraction(err)
+        worst = slack if worst is None else min(worst, slack)
+        assert slack > 0
