@@ -412,7 +412,7 @@ __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n
     if (e >= N * k16) return;
     const int64_t p = e / k16;
     const int t = (int)(e - p * k16);
-    pts16[e] = t < n ? __double2half(S * (pts[p * n_pad + t] - mn[t])) : __float2half(0.f);
+    pts16[g16(p, t, k16)] = t < n ? __double2half(S * (pts[p * n_pad + t] - mn[t])) : __float2half(0.f);
 }
 
 // norm16[p] = ||x^_p||^2 exactly (fp64), R2 = max over p, and the candidate-side
@@ -422,18 +422,17 @@ __global__ void k_norm16(int64_t N, int n, int k16, __half* __restrict__ pts16, 
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double nrm = 0.0;
     if (p < N) {
-        __half* row = pts16 + p * k16;
         for (int t = 0; t < n; ++t) {
-            const double hd = (double)__half2float(row[t]);
+            const double hd = (double)__half2float(pts16[g16(p, t, k16)]);
             nrm += hd * hd;
         }
         norm16[p] = nrm;
         const double h = -0.5 * nrm;
         const __half hh = __double2half(h);
-        row[k16 - 4] = __float2half(1.f);
-        row[k16 - 3] = __float2half(1.f);
-        row[k16 - 2] = hh;
-        row[k16 - 1] = __double2half(h - (double)__half2float(hh));
+        pts16[g16(p, k16 - 4, k16)] = __float2half(1.f);
+        pts16[g16(p, k16 - 3, k16)] = __float2half(1.f);
+        pts16[g16(p, k16 - 2, k16)] = hh;
+        pts16[g16(p, k16 - 1, k16)] = __double2half(h - (double)__half2float(hh));
     }
     unsigned long long bits = (unsigned long long)__double_as_longlong(nrm);
 #pragma unroll
@@ -458,7 +457,11 @@ static int make_fp16(Index* ix, bool* ok) {
     ix->tc_scale = std::ldexp(1.0, (int)std::floor(std::log2(180.0 / span)));
     ix->k16 = (ix->n + 4 + 15) & ~15;
     const int64_t N = ix->N;
-    GJ_CUDA(cudaMallocAsync(&ix->pts16, (size_t)N * ix->k16 * sizeof(__half), s));
+    // rows padded to a multiple of 8 plus one 128-row block of zeros: block loads
+    // that start at a row multiple of 8 never read past the allocation
+    const size_t rows16 = (size_t)((N + 7) & ~7ll) + 128;
+    GJ_CUDA(cudaMallocAsync(&ix->pts16, rows16 * ix->k16 * sizeof(__half), s));
+    GJ_CUDA(cudaMemsetAsync(ix->pts16, 0, rows16 * ix->k16 * sizeof(__half), s));
     GJ_CUDA(cudaMallocAsync(&ix->norm16, (size_t)N * sizeof(double), s));
     unsigned long long* d_r2 = nullptr;
     GJ_CUDA(cudaMallocAsync(&d_r2, sizeof(*d_r2), s));

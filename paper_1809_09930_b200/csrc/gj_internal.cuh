@@ -130,6 +130,16 @@ struct JoinParams {
 };
 JoinParams join_params(const Index* ix);
 
+// Grouped core-matrix layout of the fp16 operand array (Index::pts16): element
+// (p, k) of the logical [N][K] matrix sits at halves offset
+//   (p / 8) * 8K + (k / 8) * 64 + (p % 8) * 8 + (k % 8)
+// i.e. every 8-row group is K/8 consecutive 8x8 "core matrices" of 128 B -- the
+// canonical K-major SWIZZLE_NONE UMMA layout -- so 128 consecutive rows starting
+// at a multiple of 8 are one contiguous 128*K*2-byte block (one bulk copy).
+__host__ __device__ __forceinline__ size_t g16(size_t p, int k, int K) {
+    return (p >> 3) * (size_t)(8 * K) + (size_t)((k >> 3) * 64 + (int)(p & 7) * 8 + (k & 7));
+}
+
 // Query-side augmented MMA columns (r_hi, r_lo) of the tensor-core bound:
 // r = (T - ||q^||^2) / 2 split into fp16 hi + lo; invalid rows get the
 // sentinel -65504 so that every accumulator of the row is negative.

@@ -125,11 +125,10 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
             const int row = 32 * warp + 16 * mt + gq + 8 * h;
             const bool valid = row < (int)nq;
             const uint32_t prow = q0 + (valid ? row : 0);
-            const __half* src = P.pts16 + (size_t)prow * KP + 2 * tq;
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
-                af[mt][ks][h] = *reinterpret_cast<const uint32_t*>(src + 16 * ks);
-                af[mt][ks][2 + h] = *reinterpret_cast<const uint32_t*>(src + 16 * ks + 8);
+                af[mt][ks][h] = *reinterpret_cast<const uint32_t*>(P.pts16 + g16(prow, 16 * ks + 2 * tq, KP));
+                af[mt][ks][2 + h] = *reinterpret_cast<const uint32_t*>(P.pts16 + g16(prow, 16 * ks + 8 + 2 * tq, KP));
             }
             if (tq >= 2) {
                 __half2 aug;
@@ -201,7 +200,7 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
                 const int row = i / CH, ch = i - row * CH;
                 __half* dst = &Bs[buf][row * RS + ch * 8];
                 if (row < cnt) {
-                    cp_async16(dst, P.pts16 + (size_t)(start + row) * KP + ch * 8);
+                    cp_async16(dst, P.pts16 + g16(start + row, ch * 8, KP));
                 } else {   // padding candidate: zeros, h_hi = -65504 -> every accumulator < 0
                     union { uint4 u; __half h[8]; } c;
                     c.u = make_uint4(0, 0, 0, 0);

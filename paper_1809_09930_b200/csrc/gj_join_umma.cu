@@ -3,16 +3,11 @@
 // FP64 decision of every surviving pair (B200-first variant of PAPER.md
 // Alg. 1 l.596-607; FP64 semantics unchanged).
 //
-// CTA = 256 threads = one 128-query tile of one cell.  The tile's fp16
-// operand rows (A, M = 128) sit in shared memory in the canonical K-major
-// UMMA layout for the whole CTA lifetime.  The candidates of every adjacent
-// cell's SORTIDU window stream through a 3-buffer cp.async ring of
-// 128-candidate blocks (B, N = 128).  Thread 0 issues, per block, K/16
-// tcgen05.mma into one of two 128-column TMEM accumulators and commits to an
-// mbarrier; while the tensor core works on block kb, all 8 warps run the
-// epilogue of block kb-1: tcgen05.ld (warp w reads TMEM lanes 32(w%4).. and
-// columns 64(w/4)..), v = ||c^||^2 - 2 acc, survivor iff v <= thr - ||q^||^2,
-// and the rare survivors are decided in FP64 and emitted.
+// CTA = 6 warps = one 128-query tile of one cell (M = 128 TMEM lanes),
+// candidates in blocks of N = 128 (see k_join_umma below for the roles).
+// The fp16 operands carry augmented columns so that every accumulator is
+// (T - ||q^ - c^||^2) / 2 (gj_index.cu tc_threshold_from): a pair survives the
+// bound iff its accumulator is > +0, and survivors are decided in FP64.
 #include "gj_internal.cuh"
 #include "gj_umma.cuh"
 
@@ -21,14 +16,7 @@ namespace {
 
 constexpr int kM = 128;         // queries per tile (UMMA M)
 constexpr int kN = 128;         // candidates per block (UMMA N)
-constexpr int kThreads = 256;   // 8 warps
-// B ring depth: as many 128-candidate stages as fit next to the A tile in
-// ~100 KB (two CTAs per SM), at least 3; prefetch distance = stages - 1.
-template <int KP>
-constexpr int stages() {
-    return (100 * 1024 - kM * KP * 2) / (kN * KP * 2) < 3 ? 3 : ((100 * 1024 - kM * KP * 2) / (kN * KP * 2) > 8 ? 8 : (100 * 1024 - kM * KP * 2) / (kN * KP * 2));
-}
-
+// FP64 decision of one pair: the FP64 kernel's arithmetic (gj_join.cu).
 __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const double* __restrict__ b,
                                              int n_pad) {
     double acc = 0.0;
@@ -46,6 +34,7 @@ __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const
     return acc;
 }
 
+// Survivor of the bound: FP64 decision and emission (both orders when symmetric).
 template <int MODE, bool SYM>
 __device__ __noinline__ unsigned long long decide_and_emit(const JoinParams& P, const JoinArgs& A, uint32_t qpos,
                                                          uint32_t cpos) {
@@ -64,24 +53,43 @@ __device__ __noinline__ unsigned long long decide_and_emit(const JoinParams& P, 
     return kMul;
 }
 
+constexpr int kWarpsWs = 6;             // 0 producer, 1 MMA issuer, 2..5 epilogue
+constexpr int kThreadsWs = 32 * kWarpsWs;
+constexpr int kMaxWin = 1024;            // adjacent cells handled per setup round
 template <int KP>
-struct Smem {
-    alignas(128) __half a[kM * KP];
-    alignas(128) __half b[stages<KP>()][kN * KP];
-    uint64_t mbar[2];
+constexpr int ws_stages() { return KP <= 64 ? 4 : 3; }
+
+template <int KP>
+struct WsSmem {
+    alignas(128) __half a[kM * KP];                       // queries (A), canonical K-major layout
+    alignas(128) __half b[ws_stages<KP>()][kN * KP];      // candidate ring (B)
+    uint64_t full[ws_stages<KP>()], empty[ws_stages<KP>()], accf[2], acce[2];
     uint32_t tmem_base;
-    uint32_t win[2];
-    unsigned long long red[kThreads / 32];
+    uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];      // window [r, s), blocks (bit 31: own cell)
+    unsigned long long red[kWarpsWs];
 };
 
+// Warp-specialised tcgen05 join.  Per tile: the epilogue warps build the A
+// tile (coordinates + augmented columns r_hi, r_lo, 1, 1); all warps compute
+// the SORTIDU windows of the adjacent cells (thread per cell); then
+//   producer  : per 128-candidate block, one cp.async.bulk of the contiguous
+//               grouped-layout rows [8*floor(r/8) + 128 b, +128) into the ring
+//               (full/empty mbarriers, transaction bytes);
+//   MMA       : one thread, K/16 tcgen05.mma per block into one of two TMEM
+//               accumulators, commits to empty[stage] and acc_full[acc];
+//   epilogue  : 4 warps = 128 TMEM lanes = the tile's queries; tcgen05.ld,
+//               AND of the sign bits (survivor iff acc > +0), release the
+//               accumulator, then FP64 decision of the rare survivors whose
+//               candidate lies in [r, s) (and after the query in its own cell).
 template <int KP, int MODE, bool SYM>
-__global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A) {
+__global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem<KP>& S = *reinterpret_cast<Smem<KP>*>(smem_raw);
+    WsSmem<KP>& S = *reinterpret_cast<WsSmem<KP>*>(smem_raw);
     constexpr int KS = KP / 16;
-    constexpr int kBufs = stages<KP>();
+    constexpr int ST = ws_stages<KP>();
     constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, kN);
-    constexpr uint32_t kSBO = KP * 16;   // bytes between 8-row groups
+    constexpr uint32_t kSBO = KP * 16;
+    constexpr uint32_t kBlockBytes = kN * KP * 2;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int split = A.split > 1 ? A.split : 1;
@@ -94,42 +102,35 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
-    // ---- setup: TMEM (warp 0), mbarriers (thread 0), the A tile (all)
-    if (warp == 0) umma::tmem_alloc(&S.tmem_base, 2 * kN);
+    if (warp == 1) umma::tmem_alloc(&S.tmem_base, 2 * kN);
     if (tid == 0) {
-        umma::mbar_init(&S.mbar[0], 1);
-        umma::mbar_init(&S.mbar[1], 1);
+        for (int i = 0; i < ST; ++i) {
+            umma::mbar_init(&S.full[i], 1);
+            umma::mbar_init(&S.empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            umma::mbar_init(&S.accf[i], 1);
+            umma::mbar_init(&S.acce[i], 4);
+        }
         umma::mbar_fence_init();
     }
-    const uint32_t a_s = umma::smem_u32(S.a);
-    unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a);
-    for (int i = tid; i < kM * (KP / 8); i += kThreads) {
-        const int row = i / (KP / 8), kc = i % (KP / 8);
-        const uint32_t off = umma::tile_off(row, kc * 8, KP);
+    if (warp >= 2) {   // A tile: thread = query row
+        const int row = tid - 64;
         const bool valid = row < (int)nq;
-        if (kc < KP / 8 - 1) {
-            if (valid) umma::cp_async16(a_s + off, P.pts16 + (size_t)(q0 + row) * KP + kc * 8);
-            else *reinterpret_cast<uint4*>(a_raw + off) = make_uint4(0, 0, 0, 0);
-        } else {   // last chunk: coordinates (if any) + query-side augmented columns (r_hi, r_lo, 1, 1)
+        unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a);
+        for (int kc = 0; kc < KP / 8; ++kc) {
             union { uint4 u; __half h[8]; } c;
-            c.u = valid ? *reinterpret_cast<const uint4*>(P.pts16 + (size_t)(q0 + row) * KP + kc * 8) : make_uint4(0, 0, 0, 0);
-            query_aug(P.thr16, valid ? P.norm16[q0 + row] : 0.0, valid, c.h[4], c.h[5]);
-            c.h[6] = __float2half(1.f);
-            c.h[7] = __float2half(1.f);
-            *reinterpret_cast<uint4*>(a_raw + off) = c.u;
+            c.u = valid ? *reinterpret_cast<const uint4*>(P.pts16 + g16(q0 + row, kc * 8, KP)) : make_uint4(0, 0, 0, 0);
+            if (kc == KP / 8 - 1) {   // query-side augmented columns
+                query_aug(P.thr16, valid ? P.norm16[q0 + row] : 0.0, valid, c.h[4], c.h[5]);
+                c.h[6] = __float2half(1.f);
+                c.h[7] = __float2half(1.f);
+            }
+            *reinterpret_cast<uint4*>(a_raw + umma::tile_off(row, kc * 8, KP)) = c.u;
         }
     }
-    umma::cp_async_commit();
-    // this thread's epilogue row (TMEM lane) and column half
-    const int erow = 32 * (warp & 3) + lane;
-    const int ecol0 = 64 * (warp >> 2);
-    umma::fence_before();
-    __syncthreads();
-    umma::fence_after();
-    const uint32_t tmem = S.tmem_base;
-
     unsigned long long npairs = 0;
-    if (SYM && part == 0) {   // the self pair (q, q)
+    if (SYM && part == 0 && tid < kM) {   // the self pair (q, q); warps 0..3 cover the 128 queries
         const bool active = tid < (int)nq;
         const uint32_t qid = P.orig[q0 + (active ? tid : 0)];
         if (MODE == kEmit) {
@@ -145,121 +146,142 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
             npairs += 1;
         }
     }
+    umma::fence_proxy_async();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tmem = S.tmem_base;
 
-    uint32_t phase[2] = {0, 0};
     const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
     const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
-    for (uint32_t nbi = nb0; nbi < nb1; ++nbi) {
-        const uint32_t B = P.nbr[nbi];
-        uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
-        __syncthreads();   // previous window fully consumed (buffers, S.win)
-        if (P.sortidu) {   // tile-level SORTIDU window (exact predicates on the fp64 u-coordinates)
-            if (tid < 2) {
+    uint32_t cnt = 0;   // blocks consumed so far (identical sequence in every role)
+    const int erow = 32 * (warp & 3) + lane;   // epilogue: TMEM lane = query row
+    for (uint32_t w0 = nb0; w0 < nb1; w0 += kMaxWin) {
+        const int nwin = (int)min((uint32_t)kMaxWin, nb1 - w0);
+        for (int i = tid; i < nwin; i += kThreadsWs) {   // windows of this round (thread per adjacent cell)
+            const uint32_t B = P.nbr[w0 + i];
+            uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
+            if (P.sortidu) {
                 uint32_t lo = r, hi = s;
-                while (lo < hi) {
-                    uint32_t mid = (lo + hi) >> 1;
-                    double cu = P.pts[(size_t)mid * n_pad + P.u];
-                    bool pred = tid == 0 ? (u_lo - cu <= eps) : (cu - u_hi > eps);
-                    if (pred) hi = mid; else lo = mid + 1;
+                while (lo < hi) {   // first r with u_lo - r(u) <= eps
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (u_lo - P.pts[(size_t)mid * n_pad + P.u] <= eps) hi = mid; else lo = mid + 1;
                 }
-                S.win[tid] = lo;
+                const uint32_t rr = lo;
+                hi = s;
+                while (lo < hi) {   // first s with s(u) - u_hi > eps
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (P.pts[(size_t)mid * n_pad + P.u] - u_hi > eps) hi = mid; else lo = mid + 1;
+                }
+                r = rr;
+                s = lo;
             }
-            __syncthreads();
-            r = S.win[0];
-            s = max(S.win[1], r);
+            const bool diag = SYM && B == g;
+            if (diag) r = max(r, q0 + 1);
+            if (split > 1 && s > r) {
+                const uint64_t len = s - r;
+                s = r + (uint32_t)(len * (part + 1) / split);
+                r = r + (uint32_t)(len * part / split);
+            }
+            S.wr[i] = r;
+            S.ws[i] = s;
+            S.nbk[i] = (s > r ? (s - (r & ~7u) + kN - 1) / kN : 0u) | (diag ? 0x80000000u : 0u);
         }
-        const bool diag = SYM && B == g;
-        if (diag) r = max(r, q0 + 1);
-        if (split > 1 && s > r) {
-            const uint64_t len = s - r;
-            s = r + (uint32_t)(len * (part + 1) / split);
-            r = r + (uint32_t)(len * part / split);
-        }
-        if (s <= r) continue;
-        const int nblk = (int)((s - r + kN - 1) / kN);
-
-        auto load_block = [&](int kb) {
-            const int buf = kb % kBufs;
-            const uint32_t start = r + (uint32_t)kb * kN;
-            const int cnt = (int)min((uint32_t)kN, s - start);
-            const uint32_t b_s = umma::smem_u32(S.b[buf]);
-            for (int i = tid; i < kN * (KP / 8); i += kThreads) {
-                const int row = i / (KP / 8), kc = i % (KP / 8);
-                const uint32_t off = umma::tile_off(row, kc * 8, KP);
-                if (row < cnt) {
-                    umma::cp_async16(b_s + off, P.pts16 + (size_t)(start + row) * KP + kc * 8);
-                } else {   // padding candidate: zeros, h_hi = -65504 -> every accumulator < 0
-                    union { uint4 u; __half h[8]; } c;
-                    c.u = make_uint4(0, 0, 0, 0);
-                    if (kc == KP / 8 - 1) c.h[6] = __float2half(-65504.f);
-                    *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(S.b[buf]) + off) = c.u;
+        __syncthreads();
+        if (warp == 0) {   // ---------------- producer
+            if (lane == 0) {
+                uint32_t c = cnt;
+                for (int i = 0; i < nwin; ++i) {
+                    const uint32_t nb = S.nbk[i] & 0x7fffffffu, rb = S.wr[i] & ~7u;
+                    for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
+                        const uint32_t st = c % ST, ph = (c / ST) & 1u;
+                        umma::mbar_wait(&S.empty[st], ph ^ 1u);
+                        umma::mbar_arrive_expect_tx(&S.full[st], kBlockBytes);
+                        umma::bulk_g2s(umma::smem_u32(S.b[st]), P.pts16 + (size_t)(rb + bi * kN) * KP, kBlockBytes,
+                                       &S.full[st]);
+                    }
                 }
             }
-        };
-        auto epilogue = [&](int kb) {
-            const int ab = kb & 1;
-            umma::mbar_wait(&S.mbar[ab], phase[ab]);
-            phase[ab] ^= 1u;
-            umma::fence_after();
-            const uint32_t cbase = r + (uint32_t)kb * kN;
-            // acc = (T - ||q^ - c^||^2) / 2 + err: a pair survives iff acc > +0 (sign bit clear)
-            float v[2][32];
+        } else if (warp == 1) {   // ---------------- MMA issuer
+            if (lane == 0) {
+                uint32_t c = cnt;
+                const uint32_t a_s = umma::smem_u32(S.a);
+                for (int i = 0; i < nwin; ++i) {
+                    const uint32_t nb = S.nbk[i] & 0x7fffffffu;
+                    for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
+                        const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c & 1u, aph = (c >> 1) & 1u;
+                        umma::mbar_wait(&S.acce[ab], aph ^ 1u);
+                        umma::mbar_wait(&S.full[st], ph);
+                        umma::fence_after();
+                        const uint32_t b_s = umma::smem_u32(S.b[st]);
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-                umma::tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(ab * kN + ecol0 + 32 * h), v[h]);
-            uint32_t all = 0xffffffffu;
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int i = 0; i < 32; ++i) all &= __float_as_uint(v[h][i]);
-            unsigned long long mask = 0;
-            if (!(all >> 31)) {   // rare: some accumulator non-negative
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (!(__float_as_uint(v[h][i]) >> 31)) mask |= 1ull << (32 * h + i);
+                        for (int ks = 0; ks < KS; ++ks)
+                            umma::mma_f16(tmem + ab * kN, umma::smem_desc(a_s + ks * 256, 128, kSBO),
+                                          umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
+                        umma::commit(&S.empty[st]);
+                        umma::commit(&S.accf[ab]);
+                    }
+                }
             }
-            umma::fence_before();
-            while (mask) {   // rare: FP64 decision of the survivors
-                const int bit = __ffsll((long long)mask) - 1;
-                mask &= mask - 1;
-                const uint32_t qpos = q0 + erow, cpos = cbase + ecol0 + bit;
-                if (diag && cpos <= qpos) continue;
-                npairs += decide_and_emit<MODE, SYM>(P, A, qpos, cpos);
-            }
-        };
-
+        } else {   // ---------------- epilogue (warps 2..5)
+            uint32_t c = cnt;
+            const uint32_t qpos = q0 + erow;
+            const bool rvalid = erow < (int)nq;
+            const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+            for (int i = 0; i < nwin; ++i) {
+                const uint32_t nbw = S.nbk[i], nb = nbw & 0x7fffffffu, rb = S.wr[i] & ~7u;
+                const uint32_t wr = S.wr[i], wsd = S.ws[i];
+                const bool diag = (nbw >> 31) != 0;
+                for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
+                    const uint32_t ab = c & 1u, aph = (c >> 1) & 1u;
+                    umma::mbar_wait(&S.accf[ab], aph);
+                    umma::fence_after();
+                    unsigned long long mask[2] = {0, 0};
 #pragma unroll
-        for (int p = 0; p < kBufs - 1; ++p) {   // prologue: prefetch kBufs-1 blocks
-            if (p < nblk) load_block(p);
-            umma::cp_async_commit();
+                    for (int hh = 0; hh < 2; ++hh) {
+                        float v[2][32];
+                        umma::tmem_ld32(tmem + lane_off + ab * kN + 64 * hh, v[0]);
+                        umma::tmem_ld32(tmem + lane_off + ab * kN + 64 * hh + 32, v[1]);
+                        uint32_t all = 0xffffffffu;
+#pragma unroll
+                        for (int x = 0; x < 2; ++x)
+#pragma unroll
+                            for (int y = 0; y < 32; ++y) all &= __float_as_uint(v[x][y]);
+                        if (!(all >> 31)) {
+#pragma unroll
+                            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                                for (int y = 0; y < 32; ++y)
+                                    if (!(__float_as_uint(v[x][y]) >> 31)) mask[hh] |= 1ull << (32 * x + y);
+                        }
+                    }
+                    umma::fence_before();
+                    __syncwarp();
+                    if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                    if (!rvalid) continue;
+                    const uint32_t base = rb + bi * kN;
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        unsigned long long m = mask[hh];
+                        while (m) {   // rare: FP64 decision of the survivors
+                            const int bit = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            const uint32_t cpos = base + 64 * hh + bit;
+                            if (cpos < wr || cpos >= wsd || (diag && cpos <= qpos)) continue;
+                            npairs += decide_and_emit<MODE, SYM>(P, A, qpos, cpos);
+                        }
+                    }
+                }
+            }
         }
-        for (int kb = 0; kb < nblk; ++kb) {
-            umma::cp_async_wait<kBufs - 2>();   // block kb (and the A tile) landed; later ones may be in flight
-            umma::fence_proxy_async();
-            __syncthreads();
-            if (tid == 0) {
-                umma::fence_after();
-                const uint32_t a0 = a_s, b0 = umma::smem_u32(S.b[kb % kBufs]);
-                const uint32_t d = tmem + (uint32_t)((kb & 1) * kN);
-#pragma unroll
-                for (int ks = 0; ks < KS; ++ks)
-                    umma::mma_f16(d, umma::smem_desc(a0 + ks * 256, 128, kSBO), umma::smem_desc(b0 + ks * 256, 128, kSBO),
-                                  kIdesc, ks > 0 ? 1u : 0u);
-                umma::commit(&S.mbar[kb & 1]);
-            }
-            if (kb >= 1) epilogue(kb - 1);   // overlaps MMA(kb)
-            if (kb + kBufs - 1 < nblk) load_block(kb + kBufs - 1);   // buffer of block kb-1 (its MMA completed)
-            umma::cp_async_commit();
-        }
-        epilogue(nblk - 1);
+        // every role walked the same block sequence
+        for (int i = 0; i < nwin; ++i) cnt += S.nbk[i] & 0x7fffffffu;
+        __syncthreads();
     }
-    umma::cp_async_wait<0>();
     umma::fence_before();
     __syncthreads();
-    if (warp == 0) umma::tmem_dealloc(tmem, 2 * kN);
+    if (warp == 1) umma::tmem_dealloc(tmem, 2 * kN);
 
     if (MODE == kCount) {
         unsigned long long x = npairs;
@@ -269,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_join_umma(JoinParams P, JoinArgs A
         __syncthreads();
         if (tid == 0) {
             unsigned long long t = 0;
-            for (int w = 0; w < kThreads / 32; ++w) t += S.red[w];
+            for (int w = 0; w < kWarpsWs; ++w) t += S.red[w];
             if (t) atomicAdd((unsigned long long*)A.count, t);
             if (part == 0) atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
         }
@@ -326,10 +348,8 @@ __global__ void __launch_bounds__(128) k_umma_selftest(const __half* __restrict_
 template <int KP>
 int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
-    // request enough dynamic smem that at most 2 CTAs share an SM: the two
-    // CTAs' 2 x 256 TMEM columns fill the SM's 512
-    const size_t smem = std::max<size_t>(sizeof(Smem<KP>), 80 * 1024);
-    static_assert(sizeof(Smem<KP>) <= 227 * 1024, "shared memory");
+    const size_t smem = sizeof(WsSmem<KP>);
+    static_assert(sizeof(WsSmem<KP>) <= 227 * 1024, "shared memory");
     static bool attr_done[2][2] = {{false, false}, {false, false}};
     auto setattr = [&](const void* f, int m, int y) -> int {
         if (!attr_done[m][y]) {
@@ -343,18 +363,18 @@ int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym,
     if (mode == kEmit) {
         if (sym) {
             if ((rc = setattr((const void*)k_join_umma<KP, kEmit, true>, 0, 1))) return rc;
-            k_join_umma<KP, kEmit, true><<<grid, kThreads, smem, s>>>(p, a);
+            k_join_umma<KP, kEmit, true><<<grid, kThreadsWs, smem, s>>>(p, a);
         } else {
             if ((rc = setattr((const void*)k_join_umma<KP, kEmit, false>, 0, 0))) return rc;
-            k_join_umma<KP, kEmit, false><<<grid, kThreads, smem, s>>>(p, a);
+            k_join_umma<KP, kEmit, false><<<grid, kThreadsWs, smem, s>>>(p, a);
         }
     } else {
         if (sym) {
             if ((rc = setattr((const void*)k_join_umma<KP, kCount, true>, 1, 1))) return rc;
-            k_join_umma<KP, kCount, true><<<grid, kThreads, smem, s>>>(p, a);
+            k_join_umma<KP, kCount, true><<<grid, kThreadsWs, smem, s>>>(p, a);
         } else {
             if ((rc = setattr((const void*)k_join_umma<KP, kCount, false>, 1, 0))) return rc;
-            k_join_umma<KP, kCount, false><<<grid, kThreads, smem, s>>>(p, a);
+            k_join_umma<KP, kCount, false><<<grid, kThreadsWs, smem, s>>>(p, a);
         }
     }
     count_launch();
