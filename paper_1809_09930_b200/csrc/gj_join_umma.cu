@@ -237,28 +237,27 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                     const uint32_t ab = c & 1u, aph = (c >> 1) & 1u;
                     umma::mbar_wait(&S.accf[ab], aph);
                     umma::fence_after();
-                    unsigned long long mask[2] = {0, 0};
+                    // all 128 columns in flight at once, one wait, then release the accumulator
+                    uint32_t v[4][32];
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        float v[2][32];
-                        umma::tmem_ld32(tmem + lane_off + ab * kN + 64 * hh, v[0]);
-                        umma::tmem_ld32(tmem + lane_off + ab * kN + 64 * hh + 32, v[1]);
-                        uint32_t all = 0xffffffffu;
-#pragma unroll
-                        for (int x = 0; x < 2; ++x)
-#pragma unroll
-                            for (int y = 0; y < 32; ++y) all &= __float_as_uint(v[x][y]);
-                        if (!(all >> 31)) {
-#pragma unroll
-                            for (int x = 0; x < 2; ++x)
-#pragma unroll
-                                for (int y = 0; y < 32; ++y)
-                                    if (!(__float_as_uint(v[x][y]) >> 31)) mask[hh] |= 1ull << (32 * x + y);
-                        }
-                    }
+                    for (int x = 0; x < 4; ++x) umma::tmem_ld32_nowait(tmem + lane_off + ab * kN + 32 * x, v[x]);
+                    umma::tmem_wait_ld();
                     umma::fence_before();
                     __syncwarp();
                     if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                    uint32_t all = 0xffffffffu;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x)
+#pragma unroll
+                        for (int y = 0; y < 32; ++y) all &= v[x][y];
+                    unsigned long long mask[2] = {0, 0};
+                    if (!(all >> 31)) {   // rare: some accumulator > +0
+#pragma unroll
+                        for (int x = 0; x < 4; ++x)
+#pragma unroll
+                            for (int y = 0; y < 32; ++y)
+                                if (!(v[x][y] >> 31)) mask[x >> 1] |= 1ull << (32 * (x & 1) + y);
+                    }
                     if (!rvalid) continue;
                     const uint32_t base = rb + bi * kN;
 #pragma unroll
@@ -348,7 +347,8 @@ __global__ void __launch_bounds__(128) k_umma_selftest(const __half* __restrict_
 template <int KP>
 int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
-    const size_t smem = sizeof(WsSmem<KP>);
+    // at most two CTAs per SM: their 2 x 256 TMEM columns fill the SM's 512
+    const size_t smem = std::max<size_t>(sizeof(WsSmem<KP>), 80 * 1024);
     static_assert(sizeof(WsSmem<KP>) <= 227 * 1024, "shared memory");
     static bool attr_done[2][2] = {{false, false}, {false, false}};
     auto setattr = [&](const void* f, int m, int y) -> int {
