@@ -8,6 +8,8 @@
 // The fp16 operands carry augmented columns so that every accumulator is
 // (T - ||q^ - c^||^2) / 2 (gj_index.cu tc_threshold_from): a pair survives the
 // bound iff its accumulator is > +0, and survivors are decided in FP64.
+#include <stdlib.h>
+
 #include "gj_internal.cuh"
 #include "gj_umma.cuh"
 
@@ -56,14 +58,16 @@ __device__ __noinline__ unsigned long long decide_and_emit(const JoinParams& P, 
 constexpr int kWarpsWs = 6;             // 0 producer, 1 MMA issuer, 2..5 epilogue
 constexpr int kThreadsWs = 32 * kWarpsWs;
 constexpr int kMaxWin = 1024;            // adjacent cells handled per setup round
-template <int KP>
-constexpr int ws_stages() { return KP <= 64 ? 4 : 3; }
+// Candidate block width BN (UMMA N) and accumulator slots: 256 TMEM columns
+// per CTA (two CTAs per SM fill the 512), split into 256 / BN slots.
+template <int KP, int BN>
+constexpr int ws_stages2() { return (KP <= 64 ? 4 : 3) * (128 / BN); }
 
-template <int KP>
+template <int KP, int BN>
 struct WsSmem {
     alignas(128) __half a[kM * KP];                       // queries (A), canonical K-major layout
-    alignas(128) __half b[ws_stages<KP>()][kN * KP];      // candidate ring (B)
-    uint64_t full[ws_stages<KP>()], empty[ws_stages<KP>()], accf[2], acce[2];
+    alignas(128) __half b[ws_stages2<KP, BN>()][BN * KP]; // candidate ring (B)
+    uint64_t full[ws_stages2<KP, BN>()], empty[ws_stages2<KP, BN>()], accf[256 / BN], acce[256 / BN];
     uint32_t tmem_base;
     uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];      // window [r, s), blocks (bit 31: own cell)
     unsigned long long red[kWarpsWs];
@@ -81,15 +85,17 @@ struct WsSmem {
 //               AND of the sign bits (survivor iff acc > +0), release the
 //               accumulator, then FP64 decision of the rare survivors whose
 //               candidate lies in [r, s) (and after the query in its own cell).
-template <int KP, int MODE, bool SYM>
+template <int KP, int BN, int MODE, bool SYM>
 __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    WsSmem<KP>& S = *reinterpret_cast<WsSmem<KP>*>(smem_raw);
+    WsSmem<KP, BN>& S = *reinterpret_cast<WsSmem<KP, BN>*>(smem_raw);
     constexpr int KS = KP / 16;
-    constexpr int ST = ws_stages<KP>();
-    constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, kN);
+    constexpr int ST = ws_stages2<KP, BN>();
+    constexpr int NACC = 256 / BN;
+    constexpr int NL = BN / 32;   // 32-column TMEM loads per accumulator row
+    constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, BN);
     constexpr uint32_t kSBO = KP * 16;
-    constexpr uint32_t kBlockBytes = kN * KP * 2;
+    constexpr uint32_t kBlockBytes = BN * KP * 2;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int split = A.split > 1 ? A.split : 1;
@@ -102,13 +108,13 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
-    if (warp == 1) umma::tmem_alloc(&S.tmem_base, 2 * kN);
+    if (warp == 1) umma::tmem_alloc(&S.tmem_base, 256);
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
             umma::mbar_init(&S.full[i], 1);
             umma::mbar_init(&S.empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NACC; ++i) {
             umma::mbar_init(&S.accf[i], 1);
             umma::mbar_init(&S.acce[i], 4);
         }
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
             }
             S.wr[i] = r;
             S.ws[i] = s;
-            S.nbk[i] = (s > r ? (s - (r & ~7u) + kN - 1) / kN : 0u) | (diag ? 0x80000000u : 0u);
+            S.nbk[i] = (s > r ? (s - (r & ~7u) + BN - 1) / BN : 0u) | (diag ? 0x80000000u : 0u);
         }
         __syncthreads();
         if (warp == 0) {   // ---------------- producer
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                         const uint32_t st = c % ST, ph = (c / ST) & 1u;
                         umma::mbar_wait(&S.empty[st], ph ^ 1u);
                         umma::mbar_arrive_expect_tx(&S.full[st], kBlockBytes);
-                        umma::bulk_g2s(umma::smem_u32(S.b[st]), P.pts16 + (size_t)(rb + bi * kN) * KP, kBlockBytes,
+                        umma::bulk_g2s(umma::smem_u32(S.b[st]), P.pts16 + (size_t)(rb + bi * BN) * KP, kBlockBytes,
                                        &S.full[st]);
                     }
                 }
@@ -210,14 +216,14 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                 for (int i = 0; i < nwin; ++i) {
                     const uint32_t nb = S.nbk[i] & 0x7fffffffu;
                     for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
-                        const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c & 1u, aph = (c >> 1) & 1u;
+                        const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c % NACC, aph = (c / NACC) & 1u;
                         umma::mbar_wait(&S.acce[ab], aph ^ 1u);
                         umma::mbar_wait(&S.full[st], ph);
                         umma::fence_after();
                         const uint32_t b_s = umma::smem_u32(S.b[st]);
 #pragma unroll
                         for (int ks = 0; ks < KS; ++ks)
-                            umma::mma_f16(tmem + ab * kN, umma::smem_desc(a_s + ks * 256, 128, kSBO),
+                            umma::mma_f16(tmem + ab * BN, umma::smem_desc(a_s + ks * 256, 128, kSBO),
                                           umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
                         umma::commit(&S.empty[st]);
                         umma::commit(&S.accf[ab]);
@@ -234,34 +240,34 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                 const uint32_t wr = S.wr[i], wsd = S.ws[i];
                 const bool diag = (nbw >> 31) != 0;
                 for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
-                    const uint32_t ab = c & 1u, aph = (c >> 1) & 1u;
+                    const uint32_t ab = c % NACC, aph = (c / NACC) & 1u;
                     umma::mbar_wait(&S.accf[ab], aph);
                     umma::fence_after();
-                    // all 128 columns in flight at once, one wait, then release the accumulator
-                    uint32_t v[4][32];
+                    // all BN columns in flight at once, one wait, then release the accumulator
+                    uint32_t v[NL][32];
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) umma::tmem_ld32_nowait(tmem + lane_off + ab * kN + 32 * x, v[x]);
+                    for (int x = 0; x < NL; ++x) umma::tmem_ld32_nowait(tmem + lane_off + ab * BN + 32 * x, v[x]);
                     umma::tmem_wait_ld();
                     umma::fence_before();
                     __syncwarp();
                     if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
                     uint32_t all = 0xffffffffu;
 #pragma unroll
-                    for (int x = 0; x < 4; ++x)
+                    for (int x = 0; x < NL; ++x)
 #pragma unroll
                         for (int y = 0; y < 32; ++y) all &= v[x][y];
                     unsigned long long mask[2] = {0, 0};
                     if (!(all >> 31)) {   // rare: some accumulator > +0
 #pragma unroll
-                        for (int x = 0; x < 4; ++x)
+                        for (int x = 0; x < NL; ++x)
 #pragma unroll
                             for (int y = 0; y < 32; ++y)
                                 if (!(v[x][y] >> 31)) mask[x >> 1] |= 1ull << (32 * (x & 1) + y);
                     }
                     if (!rvalid) continue;
-                    const uint32_t base = rb + bi * kN;
+                    const uint32_t base = rb + bi * BN;
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
+                    for (int hh = 0; hh < (NL + 1) / 2; ++hh) {
                         unsigned long long m = mask[hh];
                         while (m) {   // rare: FP64 decision of the survivors
                             const int bit = __ffsll((long long)m) - 1;
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
     }
     umma::fence_before();
     __syncthreads();
-    if (warp == 1) umma::tmem_dealloc(tmem, 2 * kN);
+    if (warp == 1) umma::tmem_dealloc(tmem, 256);
 
     if (MODE == kCount) {
         unsigned long long x = npairs;
@@ -344,12 +350,12 @@ __global__ void __launch_bounds__(128) k_umma_selftest(const __half* __restrict_
     if (warp == 0) umma::tmem_dealloc(tmem, kN);
 }
 
-template <int KP>
+template <int KP, int BN>
 int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
     // at most two CTAs per SM: their 2 x 256 TMEM columns fill the SM's 512
-    const size_t smem = std::max<size_t>(sizeof(WsSmem<KP>), 80 * 1024);
-    static_assert(sizeof(WsSmem<KP>) <= 227 * 1024, "shared memory");
+    const size_t smem = std::max<size_t>(sizeof(WsSmem<KP, BN>), 80 * 1024);
+    static_assert(sizeof(WsSmem<KP, BN>) <= 227 * 1024, "shared memory");
     static bool attr_done[2][2] = {{false, false}, {false, false}};
     auto setattr = [&](const void* f, int m, int y) -> int {
         if (!attr_done[m][y]) {
@@ -362,19 +368,19 @@ int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym,
     int rc = GJ_OK;
     if (mode == kEmit) {
         if (sym) {
-            if ((rc = setattr((const void*)k_join_umma<KP, kEmit, true>, 0, 1))) return rc;
-            k_join_umma<KP, kEmit, true><<<grid, kThreadsWs, smem, s>>>(p, a);
+            if ((rc = setattr((const void*)k_join_umma<KP, BN, kEmit, true>, 0, 1))) return rc;
+            k_join_umma<KP, BN, kEmit, true><<<grid, kThreadsWs, smem, s>>>(p, a);
         } else {
-            if ((rc = setattr((const void*)k_join_umma<KP, kEmit, false>, 0, 0))) return rc;
-            k_join_umma<KP, kEmit, false><<<grid, kThreadsWs, smem, s>>>(p, a);
+            if ((rc = setattr((const void*)k_join_umma<KP, BN, kEmit, false>, 0, 0))) return rc;
+            k_join_umma<KP, BN, kEmit, false><<<grid, kThreadsWs, smem, s>>>(p, a);
         }
     } else {
         if (sym) {
-            if ((rc = setattr((const void*)k_join_umma<KP, kCount, true>, 1, 1))) return rc;
-            k_join_umma<KP, kCount, true><<<grid, kThreadsWs, smem, s>>>(p, a);
+            if ((rc = setattr((const void*)k_join_umma<KP, BN, kCount, true>, 1, 1))) return rc;
+            k_join_umma<KP, BN, kCount, true><<<grid, kThreadsWs, smem, s>>>(p, a);
         } else {
-            if ((rc = setattr((const void*)k_join_umma<KP, kCount, false>, 1, 0))) return rc;
-            k_join_umma<KP, kCount, false><<<grid, kThreadsWs, smem, s>>>(p, a);
+            if ((rc = setattr((const void*)k_join_umma<KP, BN, kCount, false>, 1, 0))) return rc;
+            k_join_umma<KP, BN, kCount, false><<<grid, kThreadsWs, smem, s>>>(p, a);
         }
     }
     count_launch();
@@ -387,15 +393,29 @@ int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym,
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     const JoinParams p = join_params(ix);
     const bool sym = ix->opt.symmetric != 0;
+    // block width: 64 candidates x 4 accumulator slots (default) or 128 x 2 (GJ_UMMA_BN=128)
+    static const int bn = [] { const char* e = getenv("GJ_UMMA_BN"); return e && atoi(e) == 128 ? 128 : 64; }();
+    if (bn == 128) {
+        switch (ix->k16) {
+            case 16: return launch_umma<16, 128>(p, mode, a, sym, s);
+            case 32: return launch_umma<32, 128>(p, mode, a, sym, s);
+            case 48: return launch_umma<48, 128>(p, mode, a, sym, s);
+            case 64: return launch_umma<64, 128>(p, mode, a, sym, s);
+            case 80: return launch_umma<80, 128>(p, mode, a, sym, s);
+            case 96: return launch_umma<96, 128>(p, mode, a, sym, s);
+            case 112: return launch_umma<112, 128>(p, mode, a, sym, s);
+            default: return launch_umma<128, 128>(p, mode, a, sym, s);
+        }
+    }
     switch (ix->k16) {
-        case 16: return launch_umma<16>(p, mode, a, sym, s);
-        case 32: return launch_umma<32>(p, mode, a, sym, s);
-        case 48: return launch_umma<48>(p, mode, a, sym, s);
-        case 64: return launch_umma<64>(p, mode, a, sym, s);
-        case 80: return launch_umma<80>(p, mode, a, sym, s);
-        case 96: return launch_umma<96>(p, mode, a, sym, s);
-        case 112: return launch_umma<112>(p, mode, a, sym, s);
-        default: return launch_umma<128>(p, mode, a, sym, s);
+        case 16: return launch_umma<16, 64>(p, mode, a, sym, s);
+        case 32: return launch_umma<32, 64>(p, mode, a, sym, s);
+        case 48: return launch_umma<48, 64>(p, mode, a, sym, s);
+        case 64: return launch_umma<64, 64>(p, mode, a, sym, s);
+        case 80: return launch_umma<80, 64>(p, mode, a, sym, s);
+        case 96: return launch_umma<96, 64>(p, mode, a, sym, s);
+        case 112: return launch_umma<112, 64>(p, mode, a, sym, s);
+        default: return launch_umma<128, 64>(p, mode, a, sym, s);
     }
 }
 
