@@ -55,8 +55,8 @@ def parse():
     p.add_argument("--no-sortidu", action="store_true")
     p.add_argument("--no-shortc", action="store_true")
     p.add_argument("--no-symmetric", action="store_true")
-    p.add_argument("--filter", type=int, default=2, choices=[0, 1, 2],
-                   help="0 FP64 scan, 1 FP32 certified prefilter, 2 tensor-core certified bound")
+    p.add_argument("--filter", type=int, default=2, choices=[0, 1, 2, 3],
+                   help="0 FP64 scan, 1 FP32 certified prefilter, 2 tcgen05 certified bound, 3 mma.sync bound")
     p.add_argument("--batch-size", type=int, default=100_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -356,12 +356,14 @@ def main():
             tj = json.load(open(tfile)).get(args.workload, {})
             traffic = tj.get(f"filter{filt}")
         scale = world if world > 1 else 1
-        if filt == 2:
+        if filt in (2, 3):
             # certified tensor-core bound: one n-dim dot product (2n flops) per
             # evaluated (unordered) candidate pair, on fp16 operands
             alg = 2.0 * n * stats["tests_evaluated"]
             peak = peaks.get("bf16_tflops_sustained", 1389.4)
-            bound, kern = "tensor", "k_join_tc (fp16 mma.sync bound + FP64 decision)"
+            bound = "tensor"
+            kern = ("k_join_umma (tcgen05/TMEM fp16 bound + FP64 decision)" if filt == 2
+                    else "k_join_tc (mma.sync fp16 bound + FP64 decision)")
             pnote = "measured cuBLAS bf16 sustained (fp16 has the same nominal dense rate)"
         else:
             # SHORTC scan: 3 flops per dimension evaluated (§4.4 "3n")
@@ -383,7 +385,8 @@ def main():
         "metric": "self-join result pairs/s", "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": {2: "f16 MMA (f32 acc) bound + f64 decision", 1: "f32 bound + f64 decision", 0: "f64"}[filt],
+        "dtype": {3: "f16 MMA (f32 acc) bound + f64 decision", 2: "f16 MMA (f32 acc) bound + f64 decision",
+                  1: "f32 bound + f64 decision", 0: "f64"}[filt],
         "data": "synthetic",
         "config": {"workload": args.workload, "generator": w["gen"], "count": N, "dims": n, "eps": w["eps"],
                    "k": w["k"], **flags, "batch_size": args.batch_size, "n_batches": nb,
