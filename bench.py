@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-symmetric", action="store_true")
     p.add_argument("--filter", type=int, default=2, choices=[0, 1, 2, 3],
                    help="0 FP64 scan, 1 FP32 certified prefilter, 2 tcgen05 certified bound, 3 mma.sync bound")
+    p.add_argument("--mma-tiles", type=int, default=0, choices=[0, 1, 2],
+                   help="filter 2: 128-query accumulator tiles per tcgen05 CTA (0 = library default, 2)")
     p.add_argument("--batch-size", type=int, default=100_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -189,7 +191,7 @@ def main():
     stream = torch.cuda.current_stream()
     w = workload(args)
     flags = dict(reorder=not args.no_reorder, sortidu=not args.no_sortidu, shortc=not args.no_shortc,
-                 symmetric=not args.no_symmetric, filter=args.filter)
+                 symmetric=not args.no_symmetric, filter=args.filter, mma_tiles=args.mma_tiles)
 
     # ---- data: generated on rank 0's host; other ranks receive it over NCCL
     N, n = w["count"], w["dims"]
@@ -395,6 +397,7 @@ def main():
                          % (N * n * 8 / 1e6)},
         "join_time_s": ms / 1000.0, "pairs": total_pairs, "selectivity": (total_pairs - N) / N,
         "index": {"n_cells": info.n_cells, "n_adjacent": info.n_adjacent, "n_tiles": info.n_tiles,
+                  "tile_queries": info.tile_queries,
                   "est_candidates": info.est_candidates},
         "phases_ms": dict(zip(["broadcast", "build_index", "estimate", "plan", "join"],
                               [float(np.mean([p[i] for p in phase_ms])) for i in range(4)] + [jms])),

@@ -70,7 +70,11 @@ typedef struct {
                             2 and 3 fall back to 1, then 0, when the data's spread makes the
                             bound uncertifiable.
                             gj_join_stats always runs the FP64 scan.                          */
-    int32_t reserved1;
+    int32_t mma_tiles;   /* filter 2 only: 128-query accumulator tiles per tcgen05 CTA that
+                            share every staged candidate block (UMMA M = 128 each):
+                            2 = query tiles of 256 points, one CTA per SM, half the candidate
+                            traffic per test (default); 1 = tiles of 128, two CTAs per SM;
+                            0 = default.  The pair set does not depend on it.               */
 } gj_options;
 
 /* Read-only description of a built index. */
@@ -83,12 +87,14 @@ typedef struct {
     double eps;
     int64_t n_cells;      /* |G|: non-empty cells (§5.6)                           */
     int64_t n_adjacent;   /* sum over cells of non-empty adjacent cells            */
-    int64_t n_tiles;      /* query tiles (<= 128 queries of one cell each)         */
+    int64_t n_tiles;      /* query tiles (<= tile_queries queries of one cell each) */
     double est_candidates;/* sum over queries of candidates before SORTIDU         */
     double build_ms;      /* device time of gj_build_index (CUDA events)           */
     int32_t filter;       /* filter the join kernel actually runs (0..3, see gj_options) */
     float filter_threshold;  /* its rejection threshold (filter 2: in scaled units)      */
     double filter_margin; /* threshold / eps^2 - 1 (relative slack of the bound)          */
+    int32_t tile_queries; /* queries per tile: 128, or 256 (filter 2 with mma_tiles = 2)  */
+    int32_t reserved;
 } gj_info;
 
 /* Work counters of one join (gj_join_stats).  cells/tests/dims/pairs are the

@@ -8,10 +8,12 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpujoin.so")
+OBJ = os.path.join(HERE, "build")
 SOURCES = ["gj_capi.cu", "gj_index.cu", "gj_join.cu", "gj_join32.cu", "gj_join_tc.cu", "gj_join_umma.cu", "gj_radix.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -27,17 +29,31 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(src: str, extra: list) -> tuple:
+    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    r = subprocess.run([NVCC, *FLAGS, *extra, "-c", "-o", obj, src], capture_output=True, text=True)
+    return obj, r
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc per translation unit (in parallel), then one shared link."""
     if not force and not stale():
         return LIB
+    os.makedirs(OBJ, exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     extra = ["-Xptxas", "-v"] if verbose else []
-    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", LIB + ".tmp", *srcs]
+    with ThreadPoolExecutor(max_workers=len(srcs)) as pool:
+        results = list(pool.map(lambda s: _compile(s, extra), srcs))
+    for obj, r in results:
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        if verbose:
+            sys.stderr.write(r.stderr)
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp",
+           *[obj for obj, _ in results]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -24,12 +24,12 @@ namespace {
 
 __global__ void k_share_queries(const uint32_t* __restrict__ tile_order, const uint32_t* __restrict__ tile_cell,
                                 const uint32_t* __restrict__ tile_q0, const uint32_t* __restrict__ cell_start,
-                                int64_t first, int64_t step, int64_t count, unsigned long long* out) {
+                                uint32_t tq, int64_t first, int64_t step, int64_t count, unsigned long long* out) {
     unsigned long long acc = 0;
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < count; m += (int64_t)gridDim.x * blockDim.x) {
         uint32_t t = tile_order[first + step * m];
         uint32_t g = tile_cell[t];
-        acc += min((uint32_t)kTileQ, cell_start[g + 1] - tile_q0[t]);
+        acc += min(tq, cell_start[g + 1] - tile_q0[t]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -91,7 +91,7 @@ using namespace gj;
 
 extern "C" {
 
-int32_t gj_abi_version(void) { return 2; }
+int32_t gj_abi_version(void) { return 3; }
 
 int64_t gj_launch_count(void) { return (int64_t)g_launches.load(); }
 
@@ -132,6 +132,7 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     ix.opt = o;
     ix.stream = (cudaStream_t)o.stream;
     if (o.filter < 0 || o.filter > 3) { set_error("filter must be 0, 1, 2 or 3"); delete h; return GJ_ERR_INVALID; }
+    if (o.mma_tiles < 0 || o.mma_tiles > 2) { set_error("mma_tiles must be 0, 1 or 2"); delete h; return GJ_ERR_INVALID; }
     ix.filter = o.filter;
     const double* dX = points;
     double* staged = nullptr;
@@ -174,6 +175,8 @@ int gj_index_info(const gj_index* h, gj_info* info) {
     info->filter = ix.filter;
     info->filter_threshold = ix.filter >= 2 ? (float)ix.thr16 : ix.thr32;
     info->filter_margin = ix.filter >= 2 ? ix.margin16 : ix.filter_margin;
+    info->tile_queries = ix.tile_q;
+    info->reserved = 0;
     return GJ_OK;
 }
 
@@ -273,7 +276,7 @@ int gj_estimate(gj_index* h, double frac, int32_t rank, int32_t world, int64_t* 
     int64_t share = rank < ix.T ? (ix.T - rank + world - 1) / world : 0;
     if (share > 0) {
         k_share_queries<<<(unsigned)std::min<int64_t>(592, (share + 255) / 256), 256, 0, s>>>(
-            ix.tile_order, ix.tile_cell, ix.tile_q0, ix.cell_start, rank, world, share,
+            ix.tile_order, ix.tile_cell, ix.tile_q0, ix.cell_start, (uint32_t)ix.tile_q, rank, world, share,
             (unsigned long long*)ix.scratch_count + 2); count_launch();
     }
     GJ_CUDA(cudaGetLastError());

@@ -286,14 +286,14 @@ __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t*
     }
 }
 
-__global__ void k_tile_count(const uint32_t* __restrict__ cell_start, int64_t G, uint32_t* __restrict__ nt) {
+__global__ void k_tile_count(const uint32_t* __restrict__ cell_start, int64_t G, uint32_t tq, uint32_t* __restrict__ nt) {
     int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < G) nt[g] = (cell_start[g + 1] - cell_start[g] + kTileQ - 1) / kTileQ;
+    if (g < G) nt[g] = (cell_start[g + 1] - cell_start[g] + tq - 1) / tq;
 }
 
 __global__ void k_tile_fill(const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ toff,
                             const uint64_t* __restrict__ cand, const uint64_t* __restrict__ cand_after, int sym,
-                            int64_t G, uint32_t* __restrict__ tile_cell,
+                            int64_t G, uint32_t tq, uint32_t* __restrict__ tile_cell,
                             uint32_t* __restrict__ tile_q0, uint64_t* __restrict__ tile_work,
                             uint64_t* __restrict__ sort_key, uint32_t* __restrict__ sort_val,
                             unsigned long long* __restrict__ total) {
@@ -301,8 +301,8 @@ __global__ void k_tile_fill(const uint32_t* __restrict__ cell_start, const uint3
     if (g >= G) return;
     uint32_t a = cell_start[g], b = cell_start[g + 1];
     uint32_t t = toff[g];
-    for (uint32_t q = a; q < b; q += kTileQ, ++t) {
-        uint32_t nq = min((uint32_t)kTileQ, b - q);
+    for (uint32_t q = a; q < b; q += tq, ++t) {
+        uint32_t nq = min(tq, b - q);
         // candidate tests of the tile: all adjacent points per query, or (symmetric)
         // points of later cells plus the later points of the own cell
         uint64_t w = sym ? (uint64_t)nq * (cand_after[g] + (b - q)) - (uint64_t)nq * (nq + 1) / 2
@@ -586,8 +586,9 @@ int build_index(Index* ix, const double* X) {
     k_adjacent<true><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, nullptr,
                                                             nullptr, nullptr, ix->nbr_off, ix->nbr, ix->nbr_self); count_launch();
     GJ_CUDA(cudaGetLastError());
-    // 8. tiles, heaviest first
-    k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, pos); count_launch();
+    // 8. tiles, heaviest first (256 queries for the two-accumulator tcgen05 kernel)
+    ix->tile_q = ix->filter == 2 ? 128 * (ix->opt.mma_tiles == 1 ? 1 : 2) : kTileQ;
+    k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, (uint32_t)ix->tile_q, pos); count_launch();
     if ((rc = scan_u32(pos, pos, G, d_tot, s))) return rc;
     GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     GJ_CUDA(cudaStreamSynchronize(s));
@@ -602,6 +603,7 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaMallocAsync(&d_total, sizeof(*d_total), s));
     GJ_CUDA(cudaMemsetAsync(d_total, 0, sizeof(*d_total), s));
     k_tile_fill<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, pos, cand, cand_after, ix->opt.symmetric, G,
+                                                   (uint32_t)ix->tile_q,
                                                    ix->tile_cell, ix->tile_q0,
                                                    ix->tile_work, skey, ix->tile_order, d_total); count_launch();
     GJ_CUDA(cudaGetLastError());

@@ -58,6 +58,7 @@ struct Index {
     __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)) + candidate-side augmented columns
     double* norm16 = nullptr;        // [N] ||fp16 coordinates||^2 (exact, fp64)
     int k16 = 0;                     // MMA depth: n + 4 augmented columns, rounded up to 16
+    int tile_q = kTileQ;             // queries per tile: 128, or 256 for the M = 2 x 128 tcgen05 kernel
     double tc_scale = 1.0;           // S, a power of two
     double thr16 = 0.0;              // tensor-core bound threshold T (scaled units)
     double margin16 = 0;             // thr16 / (S eps)^2 - 1
@@ -127,7 +128,38 @@ struct JoinParams {
     const double* __restrict__ norm16;
     int k16;
     double thr16;
+    uint32_t tile_q;                 // queries per index tile (128 or 256)
 };
+
+// The query block of one CTA.  A CTA handles `qper` queries (128, or 256 in
+// the two-accumulator tcgen05 kernel); an index tile of tile_q queries is
+// covered by tile_q / qper CTAs, and each of those by A.split candidate parts:
+//   blockIdx.x = (m * (tile_q / qper) + sub) * split + part.
+// nq = 0 marks an empty sub-block (the tile's cell ended earlier).
+struct CtaTile {
+    uint32_t g, q0, nq;
+    int part;
+};
+__device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs& A, uint32_t qper) {
+    const uint32_t split = A.split > 1 ? (uint32_t)A.split : 1u;
+    const uint32_t subs = P.tile_q > qper ? P.tile_q / qper : 1u;
+    CtaTile t;
+    t.part = (int)(blockIdx.x % split);
+    const uint32_t m = blockIdx.x / split;
+    const uint32_t sub = m % subs;
+    const int64_t j = A.first + A.step * (int64_t)(m / subs);
+    const uint32_t tile = P.tile_order[j];
+    t.g = P.tile_cell[tile];
+    t.q0 = P.tile_q0[tile] + sub * qper;
+    const uint32_t end = P.cell_start[t.g + 1];
+    t.nq = t.q0 < end ? min(qper, end - t.q0) : 0u;
+    return t;
+}
+// CTAs of a launch over a.n_tiles index tiles with `qper` queries per CTA.
+inline unsigned grid_ctas(const JoinArgs& a, int tile_q, int qper) {
+    const int64_t subs = tile_q > qper ? tile_q / qper : 1;
+    return (unsigned)(a.n_tiles * subs * (a.split > 1 ? a.split : 1));
+}
 JoinParams join_params(const Index* ix);
 
 // Grouped core-matrix layout of the fp16 operand array (Index::pts16): element

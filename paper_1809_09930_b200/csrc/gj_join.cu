@@ -64,12 +64,10 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     const unsigned lt = (1u << lane) - 1u;
     // split-K over candidates: CTA (m, part) scans part `part` of every window
     const int split = A.split > 1 ? A.split : 1;
-    const int part = (int)(blockIdx.x % split);
-    const int64_t j = A.first + A.step * (int64_t)(blockIdx.x / split);
-    const uint32_t tile = P.tile_order[j];
-    const uint32_t g = P.tile_cell[tile];
-    const uint32_t q0 = P.tile_q0[tile];
-    const uint32_t nq = min((uint32_t)kTileQ, P.cell_start[g + 1] - q0);
+    const CtaTile ct = cta_tile(P, A, kTileQ);
+    if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
+    const int part = ct.part;
+    const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
     const bool active = tid < (int)nq;
     const uint32_t qpos = q0 + (active ? tid : 0);
     const int n_pad = P.n_pad;
@@ -257,7 +255,7 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
 
 template <int NPR, bool SYM>
 void launch_mode(const Params& p, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
-    dim3 grid((unsigned)(a.n_tiles * (a.split > 1 ? a.split : 1)));
+    dim3 grid(grid_ctas(a, (int)p.tile_q, kTileQ));
     if (mode == kEmit) k_join<NPR, kEmit, SYM><<<grid, kTileQ, 0, s>>>(p, a);
     else if (mode == kCount) k_join<NPR, kCount, SYM><<<grid, kTileQ, 0, s>>>(p, a);
     else k_join<NPR, kStats, SYM><<<grid, kTileQ, 0, s>>>(p, a);
@@ -299,6 +297,7 @@ JoinParams join_params(const Index* ix) {
     p.norm16 = ix->norm16;
     p.k16 = ix->k16;
     p.thr16 = ix->thr16;
+    p.tile_q = (uint32_t)ix->tile_q;
     return p;
 }
 

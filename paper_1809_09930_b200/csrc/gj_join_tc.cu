@@ -105,12 +105,10 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gq = lane >> 2, tq = lane & 3;
     const int split = A.split > 1 ? A.split : 1;
-    const int part = (int)(blockIdx.x % split);
-    const int64_t j = A.first + A.step * (int64_t)(blockIdx.x / split);
-    const uint32_t tile = P.tile_order[j];
-    const uint32_t g = P.tile_cell[tile];
-    const uint32_t q0 = P.tile_q0[tile];
-    const uint32_t nq = min((uint32_t)kTileQ, P.cell_start[g + 1] - q0);
+    const CtaTile ct = cta_tile(P, A, kTileQ);
+    if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
+    const int part = ct.part;
+    const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
@@ -299,7 +297,7 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
 template <int KP>
 int launch_tc(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
-    dim3 grid((unsigned)(a.n_tiles * (a.split > 1 ? a.split : 1)));
+    dim3 grid(grid_ctas(a, (int)p.tile_q, kTileQ));
     if (mode == kEmit) {
         if (sym) k_join_tc<KP, kEmit, true><<<grid, kTileQ, 0, s>>>(p, a);
         else k_join_tc<KP, kEmit, false><<<grid, kTileQ, 0, s>>>(p, a);

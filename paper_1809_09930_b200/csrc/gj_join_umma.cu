@@ -36,79 +36,104 @@ __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const
     return acc;
 }
 
-// Survivor of the bound: FP64 decision and emission (both orders when symmetric).
+// FP64 decision of up to 32 staged survivors of the bound, one per lane
+// (lanes >= n idle), and emission of the pairs inside eps (both orders when
+// symmetric) with one warp-aggregated atomic.  Returns this lane's count
+// contribution (kCount).
 template <int MODE, bool SYM>
-__device__ __noinline__ unsigned long long decide_and_emit(const JoinParams& P, const JoinArgs& A, uint32_t qpos,
-                                                         uint32_t cpos) {
+__device__ __forceinline__ unsigned long long decide_batch(const JoinParams& P, const JoinArgs& A, const uint2* sv,
+                                                           uint32_t n, int lane) {
     constexpr unsigned long long kMul = SYM ? 2ull : 1ull;
-    if (dist2_fp64(P.pts + (size_t)qpos * P.n_pad, P.pts + (size_t)cpos * P.n_pad, P.n_pad) > P.eps2) return 0;
-    if (MODE == kEmit) {
-        const uint32_t qi = P.orig[qpos], ci = P.orig[cpos];
-        const unsigned long long at = atomicAdd((unsigned long long*)A.count, kMul);
+    const bool has = (uint32_t)lane < n;
+    const uint2 e = has ? sv[lane] : make_uint2(0u, 0u);
+    const bool ok = has && dist2_fp64(P.pts + (size_t)e.x * P.n_pad, P.pts + (size_t)e.y * P.n_pad, P.n_pad) <= P.eps2;
+    if (MODE != kEmit) return ok ? kMul : 0ull;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (!m) return 0ull;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd((unsigned long long*)A.count, kMul * (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ok) {
+        const unsigned long long at = base + kMul * (unsigned long long)__popc(m & ((1u << lane) - 1u));
         if (at + kMul <= A.cap) {
+            const uint32_t qi = P.orig[e.x], ci = P.orig[e.y];
             uint2* out = reinterpret_cast<uint2*>(A.out);
             out[at] = make_uint2(qi, ci);
             if (SYM) out[at + 1] = make_uint2(ci, qi);
         }
-        return 0;
     }
-    return kMul;
+    return 0ull;
 }
 
-constexpr int kWarpsWs = 6;             // 0 producer, 1 MMA issuer, 2..5 epilogue
-constexpr int kThreadsWs = 32 * kWarpsWs;
+// Tensor memory: MT accumulator blocks of 128 query rows share every
+// candidate block (MT = 2: M = 2 x 128 per B operand, so the candidate stream
+// through L2 is halved per test).  An accumulator slot is MT x BN columns;
+// 256 / BN slots; MT = 1 uses 256 columns (two CTAs per SM), MT = 2 all 512.
 constexpr int kMaxWin = 1024;            // adjacent cells handled per setup round
-// Candidate block width BN (UMMA N) and accumulator slots: 256 TMEM columns
-// per CTA (two CTAs per SM fill the 512), split into 256 / BN slots.
-template <int KP, int BN>
-constexpr int ws_stages2() { return (KP <= 64 ? 4 : 3) * (128 / BN); }
+template <int MT>
+constexpr int ws_warps() { return 2 + 4 * MT; }   // 0 producer, 1 MMA issuer, 4 x MT epilogue
+// Candidate ring depth: MT = 1 keeps two CTAs per SM; MT = 2 (one CTA per SM)
+// fills ~200 KB of shared memory beside the A tiles (latency of L2 misses).
+template <int KP, int BN, int MT>
+constexpr int ws_stages() {
+    return MT == 1 ? (KP <= 64 ? 4 : 3) * (128 / BN)
+                   : ((200 * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
+                          ? (200 * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
+                          : 24);
+}
 
-template <int KP, int BN>
+template <int KP, int BN, int MT>
 struct WsSmem {
-    alignas(128) __half a[kM * KP];                       // queries (A), canonical K-major layout
-    alignas(128) __half b[ws_stages2<KP, BN>()][BN * KP]; // candidate ring (B)
-    uint64_t full[ws_stages2<KP, BN>()], empty[ws_stages2<KP, BN>()], accf[256 / BN], acce[256 / BN];
+    alignas(128) __half a[MT][kM * KP];                       // queries (A), canonical K-major layout
+    alignas(128) __half b[ws_stages<KP, BN, MT>()][BN * KP];   // candidate ring (B)
+    uint64_t full[ws_stages<KP, BN, MT>()], empty[ws_stages<KP, BN, MT>()], accf[256 / BN], acce[256 / BN];
     uint32_t tmem_base;
-    uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];      // window [r, s), blocks (bit 31: own cell)
-    unsigned long long red[kWarpsWs];
+    uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];          // window [r, s), blocks (bit 31: own cell)
+    uint2 sv[4 * MT][64];                                     // per epilogue warp: staged survivors (qpos, cpos)
+    unsigned long long red[ws_warps<MT>()];
 };
 
-// Warp-specialised tcgen05 join.  Per tile: the epilogue warps build the A
-// tile (coordinates + augmented columns r_hi, r_lo, 1, 1); all warps compute
-// the SORTIDU windows of the adjacent cells (thread per cell); then
-//   producer  : per 128-candidate block, one cp.async.bulk of the contiguous
-//               grouped-layout rows [8*floor(r/8) + 128 b, +128) into the ring
+// Warp-specialised tcgen05 join.  Per CTA (MT x 128 queries of one cell): the
+// epilogue warps build the A tiles (coordinates + augmented columns r_hi,
+// r_lo, 1, 1); all warps compute the SORTIDU windows of the adjacent cells
+// (thread per cell, union over the CTA's queries); then
+//   producer  : per BN-candidate block, one cp.async.bulk of the contiguous
+//               grouped-layout rows [8*floor(r/8) + BN b, +BN) into the ring
 //               (full/empty mbarriers, transaction bytes);
-//   MMA       : one thread, K/16 tcgen05.mma per block into one of two TMEM
-//               accumulators, commits to empty[stage] and acc_full[acc];
-//   epilogue  : 4 warps = 128 TMEM lanes = the tile's queries; tcgen05.ld,
+//   MMA       : one thread, MT x K/16 tcgen05.mma per block (one per 128-query
+//               A tile, same B descriptor) into one accumulator slot, commits
+//               to empty[stage] and acc_full[slot];
+//   epilogue  : 4 warps per A tile = 128 TMEM lanes = its queries; tcgen05.ld,
 //               AND of the sign bits (survivor iff acc > +0), release the
-//               accumulator, then FP64 decision of the rare survivors whose
+//               slot, then FP64 decision of the rare survivors whose
 //               candidate lies in [r, s) (and after the query in its own cell).
-template <int KP, int BN, int MODE, bool SYM>
-__global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs A) {
+template <int KP, int BN, int MT, int MODE, bool SYM>
+__global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_umma(JoinParams P, JoinArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    WsSmem<KP, BN>& S = *reinterpret_cast<WsSmem<KP, BN>*>(smem_raw);
+    WsSmem<KP, BN, MT>& S = *reinterpret_cast<WsSmem<KP, BN, MT>*>(smem_raw);
+    constexpr int NW = ws_warps<MT>();
+    constexpr int NT = 32 * NW;
+    constexpr int QT = kM * MT;            // queries per CTA
+    constexpr uint32_t TCOLS = 256 * MT;   // TMEM columns allocated
     constexpr int KS = KP / 16;
-    constexpr int ST = ws_stages2<KP, BN>();
+    constexpr int ST = ws_stages<KP, BN, MT>();
     constexpr int NACC = 256 / BN;
     constexpr int NL = BN / 32;   // 32-column TMEM loads per accumulator row
     constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, BN);
     constexpr uint32_t kSBO = KP * 16;
     constexpr uint32_t kBlockBytes = BN * KP * 2;
 
+    const CtaTile ct = cta_tile(P, A, QT);
+    if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int split = A.split > 1 ? A.split : 1;
-    const int part = (int)(blockIdx.x % split);
-    const int64_t j = A.first + A.step * (int64_t)(blockIdx.x / split);
-    const uint32_t tile = P.tile_order[j];
-    const uint32_t g = P.tile_cell[tile];
-    const uint32_t q0 = P.tile_q0[tile];
-    const uint32_t nq = min((uint32_t)kM, P.cell_start[g + 1] - q0);
+    const int part = ct.part;
+    const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
+    const int nsub = (int)((nq + kM - 1) / kM);   // A tiles holding queries (1..MT)
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
-    if (warp == 1) umma::tmem_alloc(&S.tmem_base, 256);
+    if (warp == 1) umma::tmem_alloc(&S.tmem_base, TCOLS);
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
             umma::mbar_init(&S.full[i], 1);
@@ -116,14 +141,14 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
         }
         for (int i = 0; i < NACC; ++i) {
             umma::mbar_init(&S.accf[i], 1);
-            umma::mbar_init(&S.acce[i], 4);
+            umma::mbar_init(&S.acce[i], 4 * nsub);
         }
         umma::mbar_fence_init();
     }
-    if (warp >= 2) {   // A tile: thread = query row
-        const int row = tid - 64;
+    if (warp >= 2) {   // A tiles: thread = query row
+        const int row = tid - 64, sub = row >> 7, rr = row & (kM - 1);
         const bool valid = row < (int)nq;
-        unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a);
+        unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a[sub]);
         for (int kc = 0; kc < KP / 8; ++kc) {
             union { uint4 u; __half h[8]; } c;
             c.u = valid ? *reinterpret_cast<const uint4*>(P.pts16 + g16(q0 + row, kc * 8, KP)) : make_uint4(0, 0, 0, 0);
@@ -132,11 +157,11 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                 c.h[6] = __float2half(1.f);
                 c.h[7] = __float2half(1.f);
             }
-            *reinterpret_cast<uint4*>(a_raw + umma::tile_off(row, kc * 8, KP)) = c.u;
+            *reinterpret_cast<uint4*>(a_raw + umma::tile_off(rr, kc * 8, KP)) = c.u;
         }
     }
     unsigned long long npairs = 0;
-    if (SYM && part == 0 && tid < kM) {   // the self pair (q, q); warps 0..3 cover the 128 queries
+    if (SYM && part == 0 && tid < QT) {   // the self pair (q, q); warps 0..4MT-1 cover the queries
         const bool active = tid < (int)nq;
         const uint32_t qid = P.orig[q0 + (active ? tid : 0)];
         if (MODE == kEmit) {
@@ -162,10 +187,11 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
     const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
     uint32_t cnt = 0;   // blocks consumed so far (identical sequence in every role)
-    const int erow = 32 * (warp & 3) + lane;   // epilogue: TMEM lane = query row
+    const int esub = (warp - 2) >> 2;                // epilogue: A tile of this warp
+    const int erow = kM * esub + 32 * (warp & 3) + lane;   // query row; TMEM lane = erow % 128
     for (uint32_t w0 = nb0; w0 < nb1; w0 += kMaxWin) {
         const int nwin = (int)min((uint32_t)kMaxWin, nb1 - w0);
-        for (int i = tid; i < nwin; i += kThreadsWs) {   // windows of this round (thread per adjacent cell)
+        for (int i = tid; i < nwin; i += NT) {   // windows of this round (thread per adjacent cell)
             const uint32_t B = P.nbr[w0 + i];
             uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
             if (P.sortidu) {
@@ -212,7 +238,6 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
         } else if (warp == 1) {   // ---------------- MMA issuer
             if (lane == 0) {
                 uint32_t c = cnt;
-                const uint32_t a_s = umma::smem_u32(S.a);
                 for (int i = 0; i < nwin; ++i) {
                     const uint32_t nb = S.nbk[i] & 0x7fffffffu;
                     for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
@@ -222,19 +247,31 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                         umma::fence_after();
                         const uint32_t b_s = umma::smem_u32(S.b[st]);
 #pragma unroll
-                        for (int ks = 0; ks < KS; ++ks)
-                            umma::mma_f16(tmem + ab * BN, umma::smem_desc(a_s + ks * 256, 128, kSBO),
-                                          umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
+                        for (int sub = 0; sub < MT; ++sub) {
+                            if (sub >= nsub) break;
+                            const uint32_t a_s = umma::smem_u32(S.a[sub]);
+#pragma unroll
+                            for (int ks = 0; ks < KS; ++ks)
+                                umma::mma_f16(tmem + (uint32_t)((ab * MT + sub) * BN),
+                                              umma::smem_desc(a_s + ks * 256, 128, kSBO),
+                                              umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
+                        }
                         umma::commit(&S.empty[st]);
                         umma::commit(&S.accf[ab]);
                     }
                 }
             }
-        } else {   // ---------------- epilogue (warps 2..5)
+        } else if (esub < nsub) {   // ---------------- epilogue (warps 2 .. 2 + 4 nsub - 1)
             uint32_t c = cnt;
             const uint32_t qpos = q0 + erow;
             const bool rvalid = erow < (int)nq;
             const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+            const unsigned lt = (1u << lane) - 1u;
+            // Survivors of the bound are staged per warp and decided 32 at a time
+            // (one per lane), so a rare FP64 decision never holds the accumulator
+            // pipeline for a full memory round trip per pair.
+            uint2* sv = S.sv[warp - 2];
+            uint32_t svn = 0;
             for (int i = 0; i < nwin; ++i) {
                 const uint32_t nbw = S.nbk[i], nb = nbw & 0x7fffffffu, rb = S.wr[i] & ~7u;
                 const uint32_t wr = S.wr[i], wsd = S.ws[i];
@@ -245,8 +282,9 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
                     umma::fence_after();
                     // all BN columns in flight at once, one wait, then release the accumulator
                     uint32_t v[NL][32];
+                    const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN);
 #pragma unroll
-                    for (int x = 0; x < NL; ++x) umma::tmem_ld32_nowait(tmem + lane_off + ab * BN + 32 * x, v[x]);
+                    for (int x = 0; x < NL; ++x) umma::tmem_ld32_nowait(tcol + 32 * x, v[x]);
                     umma::tmem_wait_ld();
                     umma::fence_before();
                     __syncwarp();
@@ -257,27 +295,45 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
 #pragma unroll
                         for (int y = 0; y < 32; ++y) all &= v[x][y];
                     unsigned long long mask[2] = {0, 0};
-                    if (!(all >> 31)) {   // rare: some accumulator > +0
+                    if (rvalid && !(all >> 31)) {   // rare: some accumulator > +0
 #pragma unroll
                         for (int x = 0; x < NL; ++x)
 #pragma unroll
                             for (int y = 0; y < 32; ++y)
                                 if (!(v[x][y] >> 31)) mask[x >> 1] |= 1ull << (32 * (x & 1) + y);
                     }
-                    if (!rvalid) continue;
+                    if (!__any_sync(0xffffffffu, (mask[0] | mask[1]) != 0ull)) continue;
                     const uint32_t base = rb + bi * BN;
 #pragma unroll
                     for (int hh = 0; hh < (NL + 1) / 2; ++hh) {
                         unsigned long long m = mask[hh];
-                        while (m) {   // rare: FP64 decision of the survivors
-                            const int bit = __ffsll((long long)m) - 1;
-                            m &= m - 1;
-                            const uint32_t cpos = base + 64 * hh + bit;
-                            if (cpos < wr || cpos >= wsd || (diag && cpos <= qpos)) continue;
-                            npairs += decide_and_emit<MODE, SYM>(P, A, qpos, cpos);
+                        while (__any_sync(0xffffffffu, m != 0ull)) {   // stage the survivors in [r, s)
+                            uint32_t cpos = 0;
+                            bool has = false;
+                            if (m) {
+                                const int bit = __ffsll((long long)m) - 1;
+                                m &= m - 1;
+                                cpos = base + 64 * hh + bit;
+                                has = !(cpos < wr || cpos >= wsd || (diag && cpos <= qpos));
+                            }
+                            const unsigned hb = __ballot_sync(0xffffffffu, has);
+                            if (has) sv[svn + __popc(hb & lt)] = make_uint2(qpos, cpos);
+                            svn += __popc(hb);
+                            if (svn >= 32) {   // a full batch: one FP64 decision per lane
+                                __syncwarp();
+                                npairs += decide_batch<MODE, SYM>(P, A, sv, 32, lane);
+                                __syncwarp();
+                                if ((uint32_t)lane < svn - 32) sv[lane] = sv[32 + lane];
+                                svn -= 32;
+                                __syncwarp();
+                            }
                         }
                     }
                 }
+            }
+            if (svn) {   // the rest of this round's survivors
+                __syncwarp();
+                npairs += decide_batch<MODE, SYM>(P, A, sv, svn, lane);
             }
         }
         // every role walked the same block sequence
@@ -286,7 +342,7 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
     }
     umma::fence_before();
     __syncthreads();
-    if (warp == 1) umma::tmem_dealloc(tmem, 256);
+    if (warp == 1) umma::tmem_dealloc(tmem, TCOLS);
 
     if (MODE == kCount) {
         unsigned long long x = npairs;
@@ -296,7 +352,7 @@ __global__ void __launch_bounds__(kThreadsWs) k_join_umma(JoinParams P, JoinArgs
         __syncthreads();
         if (tid == 0) {
             unsigned long long t = 0;
-            for (int w = 0; w < kWarpsWs; ++w) t += S.red[w];
+            for (int w = 0; w < NW; ++w) t += S.red[w];
             if (t) atomicAdd((unsigned long long*)A.count, t);
             if (part == 0) atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
         }
@@ -350,42 +406,44 @@ __global__ void __launch_bounds__(128) k_umma_selftest(const __half* __restrict_
     if (warp == 0) umma::tmem_dealloc(tmem, kN);
 }
 
-template <int KP, int BN>
-int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
-    if (a.n_tiles <= 0) return GJ_OK;
-    // at most two CTAs per SM: their 2 x 256 TMEM columns fill the SM's 512
-    const size_t smem = std::max<size_t>(sizeof(WsSmem<KP, BN>), 80 * 1024);
-    static_assert(sizeof(WsSmem<KP, BN>) <= 227 * 1024, "shared memory");
-    static bool attr_done[2][2] = {{false, false}, {false, false}};
-    auto setattr = [&](const void* f, int m, int y) -> int {
-        if (!attr_done[m][y]) {
-            GJ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_done[m][y] = true;
-        }
-        return GJ_OK;
-    };
-    dim3 grid((unsigned)(a.n_tiles * (a.split > 1 ? a.split : 1)));
-    int rc = GJ_OK;
-    if (mode == kEmit) {
-        if (sym) {
-            if ((rc = setattr((const void*)k_join_umma<KP, BN, kEmit, true>, 0, 1))) return rc;
-            k_join_umma<KP, BN, kEmit, true><<<grid, kThreadsWs, smem, s>>>(p, a);
-        } else {
-            if ((rc = setattr((const void*)k_join_umma<KP, BN, kEmit, false>, 0, 0))) return rc;
-            k_join_umma<KP, BN, kEmit, false><<<grid, kThreadsWs, smem, s>>>(p, a);
-        }
-    } else {
-        if (sym) {
-            if ((rc = setattr((const void*)k_join_umma<KP, BN, kCount, true>, 1, 1))) return rc;
-            k_join_umma<KP, BN, kCount, true><<<grid, kThreadsWs, smem, s>>>(p, a);
-        } else {
-            if ((rc = setattr((const void*)k_join_umma<KP, BN, kCount, false>, 1, 0))) return rc;
-            k_join_umma<KP, BN, kCount, false><<<grid, kThreadsWs, smem, s>>>(p, a);
-        }
+template <int KP, int BN, int MT, int MODE, bool SYM>
+int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
+    // MT = 1: at most two CTAs per SM (their 2 x 256 TMEM columns fill the SM's 512);
+    // MT = 2: exactly one (512 columns), forced by > 114 KB of shared memory
+    const size_t smem = std::max<size_t>(sizeof(WsSmem<KP, BN, MT>), MT == 1 ? 80 * 1024 : 120 * 1024);
+    static_assert(sizeof(WsSmem<KP, BN, MT>) <= 227 * 1024, "shared memory");
+    static bool attr_done = false;
+    if (!attr_done) {
+        GJ_CUDA(cudaFuncSetAttribute((const void*)k_join_umma<KP, BN, MT, MODE, SYM>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done = true;
     }
+    k_join_umma<KP, BN, MT, MODE, SYM><<<grid_ctas(a, (int)p.tile_q, kM * MT), 32 * ws_warps<MT>(), smem, s>>>(p, a);
     count_launch();
     GJ_CUDA(cudaGetLastError());
     return GJ_OK;
+}
+
+template <int KP, int BN, int MT>
+int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
+    if (a.n_tiles <= 0) return GJ_OK;
+    if (mode == kEmit) return sym ? launch_umma_k<KP, BN, MT, kEmit, true>(p, a, s)
+                                  : launch_umma_k<KP, BN, MT, kEmit, false>(p, a, s);
+    return sym ? launch_umma_k<KP, BN, MT, kCount, true>(p, a, s) : launch_umma_k<KP, BN, MT, kCount, false>(p, a, s);
+}
+
+template <int BN, int MT>
+int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
+    switch (ix->k16) {
+        case 16: return launch_umma<16, BN, MT>(p, mode, a, sym, s);
+        case 32: return launch_umma<32, BN, MT>(p, mode, a, sym, s);
+        case 48: return launch_umma<48, BN, MT>(p, mode, a, sym, s);
+        case 64: return launch_umma<64, BN, MT>(p, mode, a, sym, s);
+        case 80: return launch_umma<80, BN, MT>(p, mode, a, sym, s);
+        case 96: return launch_umma<96, BN, MT>(p, mode, a, sym, s);
+        case 112: return launch_umma<112, BN, MT>(p, mode, a, sym, s);
+        default: return launch_umma<128, BN, MT>(p, mode, a, sym, s);
+    }
 }
 
 }  // namespace
@@ -393,30 +451,11 @@ int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym,
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     const JoinParams p = join_params(ix);
     const bool sym = ix->opt.symmetric != 0;
-    // block width: 64 candidates x 4 accumulator slots (default) or 128 x 2 (GJ_UMMA_BN=128)
-    static const int bn = [] { const char* e = getenv("GJ_UMMA_BN"); return e && atoi(e) == 128 ? 128 : 64; }();
-    if (bn == 128) {
-        switch (ix->k16) {
-            case 16: return launch_umma<16, 128>(p, mode, a, sym, s);
-            case 32: return launch_umma<32, 128>(p, mode, a, sym, s);
-            case 48: return launch_umma<48, 128>(p, mode, a, sym, s);
-            case 64: return launch_umma<64, 128>(p, mode, a, sym, s);
-            case 80: return launch_umma<80, 128>(p, mode, a, sym, s);
-            case 96: return launch_umma<96, 128>(p, mode, a, sym, s);
-            case 112: return launch_umma<112, 128>(p, mode, a, sym, s);
-            default: return launch_umma<128, 128>(p, mode, a, sym, s);
-        }
-    }
-    switch (ix->k16) {
-        case 16: return launch_umma<16, 64>(p, mode, a, sym, s);
-        case 32: return launch_umma<32, 64>(p, mode, a, sym, s);
-        case 48: return launch_umma<48, 64>(p, mode, a, sym, s);
-        case 64: return launch_umma<64, 64>(p, mode, a, sym, s);
-        case 80: return launch_umma<80, 64>(p, mode, a, sym, s);
-        case 96: return launch_umma<96, 64>(p, mode, a, sym, s);
-        case 112: return launch_umma<112, 64>(p, mode, a, sym, s);
-        default: return launch_umma<128, 64>(p, mode, a, sym, s);
-    }
+    // block width: 128 candidates (default) or 64 (GJ_UMMA_BN=64); A tiles per CTA = tile_q / 128
+    static const int bn = [] { const char* e = getenv("GJ_UMMA_BN"); return e && atoi(e) == 64 ? 64 : 128; }();
+    const int mt = ix->tile_q / kM;
+    if (mt == 1) return bn == 64 ? launch_umma_kp<64, 1>(ix, p, mode, a, sym, s) : launch_umma_kp<128, 1>(ix, p, mode, a, sym, s);
+    return bn == 64 ? launch_umma_kp<64, 2>(ix, p, mode, a, sym, s) : launch_umma_kp<128, 2>(ix, p, mode, a, sym, s);
 }
 
 int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s) {

@@ -27,14 +27,15 @@ EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_orde
 class Options(C.Structure):
     _fields_ = [("reorder", C.c_int32), ("sortidu", C.c_int32), ("shortc", C.c_int32), ("symmetric", C.c_int32),
                 ("sample_frac", C.c_double), ("stream", C.c_uint64), ("filter", C.c_int32),
-                ("reserved1", C.c_int32)]
+                ("mma_tiles", C.c_int32)]
 
 
 class Info(C.Structure):
     _fields_ = [("n_points", C.c_int64), ("dim", C.c_int32), ("dim_pad", C.c_int32), ("k", C.c_int32),
                 ("u", C.c_int32), ("eps", C.c_double), ("n_cells", C.c_int64), ("n_adjacent", C.c_int64),
                 ("n_tiles", C.c_int64), ("est_candidates", C.c_double), ("build_ms", C.c_double),
-                ("filter", C.c_int32), ("filter_threshold", C.c_float), ("filter_margin", C.c_double)]
+                ("filter", C.c_int32), ("filter_threshold", C.c_float), ("filter_margin", C.c_double),
+                ("tile_queries", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -97,11 +98,12 @@ def _check(rc):
 
 
 def default_options(reorder=True, sortidu=True, shortc=True, sample_frac=0.01, stream=0, symmetric=True,
-                    filter=2) -> Options:
+                    filter=2, mma_tiles=0) -> Options:
     o = Options()
     lib().gj_default_options(C.byref(o))
     o.reorder, o.sortidu, o.shortc, o.symmetric = int(reorder), int(sortidu), int(shortc), int(symmetric)
     o.filter = int(filter)
+    o.mma_tiles = int(mma_tiles)
     o.sample_frac = float(sample_frac)
     o.stream = int(stream)
     return o
@@ -129,7 +131,7 @@ class Index:
     tensor (stays on the device) or a host numpy array / tensor (staged)."""
 
     def __init__(self, points, eps: float, k: int, reorder=True, sortidu=True, shortc=True, sample_frac=0.01,
-                 stream=None, symmetric=True, filter=2):
+                 stream=None, symmetric=True, filter=2, mma_tiles=0):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
@@ -141,7 +143,7 @@ class Index:
         self._keep = points
         n, dim = points.shape
         self.n_points, self.dim = int(n), int(dim)
-        self.options = default_options(reorder, sortidu, shortc, sample_frac, stream, symmetric, filter)
+        self.options = default_options(reorder, sortidu, shortc, sample_frac, stream, symmetric, filter, mma_tiles)
         h = C.c_void_p()
         _check(lib().gj_build_index(_ptr(points), n, dim, float(eps), int(k), C.byref(self.options), C.byref(h)))
         self._h = h

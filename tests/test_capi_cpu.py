@@ -44,7 +44,7 @@ def test_library_is_built_for_sm100a(L):
 
 
 def test_host_only_entry_points(L):
-    assert pkg.abi_version() == 2
+    assert pkg.abi_version() == 3
     o = gpujoin.default_options()
     assert (o.reorder, o.sortidu, o.shortc, o.symmetric, o.filter) == (1, 1, 1, 1, 2) and o.sample_frac == 0.01
     # computeNumBatches (§3.2.2 l.199-200)

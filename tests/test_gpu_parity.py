@@ -70,6 +70,21 @@ def test_filters_on_paper_shapes(filt, gen, count, dims, eps, k):
     check(D, eps, got)
 
 
+@pytest.mark.parametrize("mma_tiles", [1, 2])
+@pytest.mark.parametrize("symmetric", [0, 1])
+@pytest.mark.parametrize("gen,count,dims,eps,k", [("exponential", 7000, 32, 0.08, 6),   # few huge cells
+                                                   ("exponential", 2000, 16, 0.04, 3),   # ragged 129..255-query tails
+                                                   ("uniform", 1500, 12, 0.45, 4)])      # many small cells (< 128)
+def test_tcgen05_accumulator_tiles(mma_tiles, symmetric, gen, count, dims, eps, k):
+    """One or two 128-query accumulator tiles per tcgen05 CTA (gj_options.mma_tiles):
+    identical pair sets; tiles of 256 queries when two."""
+    D = synth.make(gen, count, dims, seed=count + dims)
+    got, ix = gpu_pairs(D, eps, k, filter=2, mma_tiles=mma_tiles, symmetric=symmetric)
+    assert ix.info().filter == 2
+    assert ix.info().tile_queries == 128 * mma_tiles
+    check(D, eps, got)
+
+
 SMALL = [  # (generator, |D|, n, eps, k)
     ("uniform", 2000, 16, 0.96, 6),       # BASELINE configs[0] (~8 neighbours/point)
     ("exponential", 3000, 16, 0.04, 6),

@@ -16,6 +16,7 @@ p.add_argument("--count", type=int, default=None)
 p.add_argument("--eps", type=float, default=None)
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--filter", type=int, default=2)
+p.add_argument("--mma-tiles", type=int, default=0)
 a = p.parse_args()
 w = dict(synth.WORKLOADS[a.workload])
 if a.count:
@@ -24,7 +25,7 @@ if a.eps:
     w["eps"] = a.eps
 D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
 for r in range(a.reps):
-    ix = Index(D, w["eps"], w["k"], filter=a.filter)
+    ix = Index(D, w["eps"], w["k"], filter=a.filter, mma_tiles=a.mma_tiles)
     est = ix.estimate(1.0)
     out = torch.empty((est + 1024, 2), dtype=torch.int32, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -33,7 +34,7 @@ for r in range(a.reps):
     ix.self_join_async(out, cnt)
     e.record()
     torch.cuda.synchronize()
-    print(f"rep {r}: filter={ix.info().filter} pairs={int(cnt.item())} join_ms={s.elapsed_time(e):.2f} "
+    print(f"rep {r}: filter={ix.info().filter} tile_q={ix.info().tile_queries} pairs={int(cnt.item())} join_ms={s.elapsed_time(e):.2f} "
           f"build_ms={ix.info().build_ms:.2f} margin={ix.info().filter_margin:.3g}",
           flush=True)
     ix.free()
