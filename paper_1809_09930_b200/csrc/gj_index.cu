@@ -457,9 +457,9 @@ static int make_fp16(Index* ix, bool* ok) {
     ix->tc_scale = std::ldexp(1.0, (int)std::floor(std::log2(180.0 / span)));
     ix->k16 = (ix->n + 4 + 15) & ~15;
     const int64_t N = ix->N;
-    // rows padded to a multiple of 8 plus one 128-row block of zeros: block loads
-    // that start at a row multiple of 8 never read past the allocation
-    const size_t rows16 = (size_t)((N + 7) & ~7ll) + 128;
+    // rows padded to a multiple of 8 plus one 256-row block of zeros: block loads
+    // (<= 256 rows) that start at a row multiple of 8 never read past the allocation
+    const size_t rows16 = (size_t)((N + 7) & ~7ll) + 256;
     GJ_CUDA(cudaMallocAsync(&ix->pts16, rows16 * ix->k16 * sizeof(__half), s));
     GJ_CUDA(cudaMemsetAsync(ix->pts16, 0, rows16 * ix->k16 * sizeof(__half), s));
     GJ_CUDA(cudaMallocAsync(&ix->norm16, (size_t)N * sizeof(double), s));

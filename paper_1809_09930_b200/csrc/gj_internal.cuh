@@ -129,6 +129,7 @@ struct JoinParams {
     int k16;
     double thr16;
     uint32_t tile_q;                 // queries per index tile (128 or 256)
+    int debug;                       // timing experiments only (GJ_DEBUG_UMMA); 0 in production
 };
 
 // The query block of one CTA.  A CTA handles `qper` queries (128, or 256 in

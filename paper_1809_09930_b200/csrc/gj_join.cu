@@ -23,6 +23,8 @@
 //
 // No tensor cores: the candidate work is a filtered gather with a
 // data-dependent early exit, not a dense contraction (north_star).
+#include <stdlib.h>
+
 #include "gj_internal.cuh"
 
 namespace gj {
@@ -298,6 +300,8 @@ JoinParams join_params(const Index* ix) {
     p.k16 = ix->k16;
     p.thr16 = ix->thr16;
     p.tile_q = (uint32_t)ix->tile_q;
+    static const int dbg = [] { const char* e = getenv("GJ_DEBUG_UMMA"); return e ? atoi(e) : 0; }();
+    p.debug = dbg;
     return p;
 }
 

@@ -3,8 +3,9 @@
 // FP64 decision of every surviving pair (B200-first variant of PAPER.md
 // Alg. 1 l.596-607; FP64 semantics unchanged).
 //
-// CTA = 6 warps = one 128-query tile of one cell (M = 128 TMEM lanes),
-// candidates in blocks of N = 128 (see k_join_umma below for the roles).
+// CTA = one producer warp, one MMA-issuer warp and 4 x EPW epilogue warps per
+// 128-query A tile of one cell (M = 128 TMEM lanes); candidates in blocks of
+// BN = 256 (default) or 128 rows (see k_join_umma below for the roles).
 // The fp16 operands carry augmented columns so that every accumulator is
 // (T - ||q^ - c^||^2) / 2 (gj_index.cu tc_threshold_from): a pair survives the
 // bound iff its accumulator is > +0, and survivors are decided in FP64.
@@ -67,30 +68,41 @@ __device__ __forceinline__ unsigned long long decide_batch(const JoinParams& P, 
 
 // Tensor memory: MT accumulator blocks of 128 query rows share every
 // candidate block (MT = 2: M = 2 x 128 per B operand, so the candidate stream
-// through L2 is halved per test).  An accumulator slot is MT x BN columns;
-// 256 / BN slots; MT = 1 uses 256 columns (two CTAs per SM), MT = 2 all 512.
-constexpr int kMaxWin = 1024;            // adjacent cells handled per setup round
-template <int MT>
-constexpr int ws_warps() { return 2 + 4 * MT; }   // 0 producer, 1 MMA issuer, 4 x MT epilogue
-// Candidate ring depth: MT = 1 keeps two CTAs per SM; MT = 2 (one CTA per SM)
-// fills ~200 KB of shared memory beside the A tiles (latency of L2 misses).
-template <int KP, int BN, int MT>
+// through L2 is halved per test).  An accumulator slot is MT x BN columns,
+// 256 / BN slots per CTA: MT = 1 uses 256 columns (two CTAs per SM, four
+// slots in flight per SM), MT = 2 all 512 (one CTA per SM).
+//
+// Epilogue: EPW warps per (A tile, 32-lane TMEM quarter), each reading BN / EPW
+// columns.  The accumulator read (4 B per candidate test against 2K MMA
+// flops) is as expensive as the MMA itself at K = 48, and TMEM read
+// throughput grows with the number of reading warps (tools/micro/tmem_ld_bw:
+// ~330 B/clk/SM with 8 warps, ~470 with 16), so MT = 1 runs EPW = 2 (16
+// epilogue warps per SM).
+constexpr int kMaxWin = 512;             // adjacent cells handled per setup round
+template <int MT, int EPW>
+constexpr int ws_warps() { return 2 + 4 * MT * EPW; }   // 0 producer, 1 MMA issuer, epilogue
+// CTAs per SM: two when a CTA's accumulator slots (MT x SL x BN columns) fit
+// in half of the SM's 512 TMEM columns.
+template <int BN, int MT, int SL>
+constexpr int ws_ctas_per_sm() { return MT * SL * BN <= 256 ? 2 : 1; }
+// Candidate ring depth: as many BN-row blocks as fit beside the A tiles in
+// ~100 KB (two CTAs per SM) or ~200 KB (one) of shared memory, at most 24.
+template <int KP, int BN, int MT, int SL>
 constexpr int ws_stages() {
-    return MT == 1 ? (KP <= 64 ? 4 : 3) * (128 / BN)
-                   : ((200 * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
-                          ? (200 * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
-                          : 24);
+    return ((ws_ctas_per_sm<BN, MT, SL>() == 2 ? 96 : 196) * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
+               ? ((ws_ctas_per_sm<BN, MT, SL>() == 2 ? 96 : 196) * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
+               : 24;
 }
 
-template <int KP, int BN, int MT>
+template <int KP, int BN, int MT, int SL, int EPW>
 struct WsSmem {
-    alignas(128) __half a[MT][kM * KP];                       // queries (A), canonical K-major layout
-    alignas(128) __half b[ws_stages<KP, BN, MT>()][BN * KP];   // candidate ring (B)
-    uint64_t full[ws_stages<KP, BN, MT>()], empty[ws_stages<KP, BN, MT>()], accf[256 / BN], acce[256 / BN];
+    alignas(128) __half a[MT][kM * KP];                           // queries (A), canonical K-major layout
+    alignas(128) __half b[ws_stages<KP, BN, MT, SL>()][BN * KP];   // candidate ring (B)
+    uint64_t full[ws_stages<KP, BN, MT, SL>()], empty[ws_stages<KP, BN, MT, SL>()], accf[SL], acce[SL];
     uint32_t tmem_base;
     uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];          // window [r, s), blocks (bit 31: own cell)
-    uint2 sv[4 * MT][64];                                     // per epilogue warp: staged survivors (qpos, cpos)
-    unsigned long long red[ws_warps<MT>()];
+    uint2 sv[4 * MT * EPW][64];                               // per epilogue warp: staged survivors (qpos, cpos)
+    unsigned long long red[ws_warps<MT, EPW>()];
 };
 
 // Warp-specialised tcgen05 join.  Per CTA (MT x 128 queries of one cell): the
@@ -103,25 +115,30 @@ struct WsSmem {
 //   MMA       : one thread, MT x K/16 tcgen05.mma per block (one per 128-query
 //               A tile, same B descriptor) into one accumulator slot, commits
 //               to empty[stage] and acc_full[slot];
-//   epilogue  : 4 warps per A tile = 128 TMEM lanes = its queries; tcgen05.ld,
-//               AND of the sign bits (survivor iff acc > +0), release the
-//               slot, then FP64 decision of the rare survivors whose
-//               candidate lies in [r, s) (and after the query in its own cell).
-template <int KP, int BN, int MT, int MODE, bool SYM>
-__global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_umma(JoinParams P, JoinArgs A) {
+//   epilogue  : 4 x EPW warps per A tile (TMEM lane quarter = warp % 4, column
+//               part BN / EPW); tcgen05.ld, AND of the sign bits (survivor iff
+//               acc > +0), release the slot, then stage the rare survivors
+//               whose candidate lies in [r, s) (and after the query in its own
+//               cell) for a lane-parallel FP64 decision.
+template <int KP, int BN, int MT, int SL, int EPW, int MODE, bool SYM>
+__global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, MT, SL>())
+    k_join_umma(JoinParams P, JoinArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    WsSmem<KP, BN, MT>& S = *reinterpret_cast<WsSmem<KP, BN, MT>*>(smem_raw);
-    constexpr int NW = ws_warps<MT>();
+    WsSmem<KP, BN, MT, SL, EPW>& S = *reinterpret_cast<WsSmem<KP, BN, MT, SL, EPW>*>(smem_raw);
+    constexpr int NE = 4 * MT * EPW;       // epilogue warps
+    constexpr int NW = ws_warps<MT, EPW>();
     constexpr int NT = 32 * NW;
     constexpr int QT = kM * MT;            // queries per CTA
-    constexpr uint32_t TCOLS = 256 * MT;   // TMEM columns allocated
+    constexpr uint32_t TCOLS = MT * SL * BN <= 256 ? 256 : 512;   // TMEM columns allocated (power of 2)
     constexpr int KS = KP / 16;
-    constexpr int ST = ws_stages<KP, BN, MT>();
-    constexpr int NACC = 256 / BN;
-    constexpr int NL = BN / 32;   // 32-column TMEM loads per accumulator row
+    constexpr int ST = ws_stages<KP, BN, MT, SL>();
+    constexpr int NACC = SL;
+    constexpr int CW = BN / EPW;           // accumulator columns per epilogue warp
+    constexpr int NL = CW / 32;            // 32-column TMEM loads per warp and block
     constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, BN);
     constexpr uint32_t kSBO = KP * 16;
     constexpr uint32_t kBlockBytes = BN * KP * 2;
+    static_assert(NL >= 1 && NL <= 4, "epilogue columns per warp");
 
     const CtaTile ct = cta_tile(P, A, QT);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
@@ -141,12 +158,12 @@ __global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_u
         }
         for (int i = 0; i < NACC; ++i) {
             umma::mbar_init(&S.accf[i], 1);
-            umma::mbar_init(&S.acce[i], 4 * nsub);
+            umma::mbar_init(&S.acce[i], 4 * EPW * nsub);
         }
         umma::mbar_fence_init();
     }
-    if (warp >= 2) {   // A tiles: thread = query row
-        const int row = tid - 64, sub = row >> 7, rr = row & (kM - 1);
+    for (int row = tid - 64; row >= 0 && row < QT; row += 32 * NE) {   // A tiles: thread = query row
+        const int sub = row >> 7, rr = row & (kM - 1);
         const bool valid = row < (int)nq;
         unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a[sub]);
         for (int kc = 0; kc < KP / 8; ++kc) {
@@ -161,7 +178,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_u
         }
     }
     unsigned long long npairs = 0;
-    if (SYM && part == 0 && tid < QT) {   // the self pair (q, q); warps 0..4MT-1 cover the queries
+    if (SYM && part == 0 && tid < QT) {   // the self pair (q, q)
         const bool active = tid < (int)nq;
         const uint32_t qid = P.orig[q0 + (active ? tid : 0)];
         if (MODE == kEmit) {
@@ -187,7 +204,8 @@ __global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_u
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
     const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
     uint32_t cnt = 0;   // blocks consumed so far (identical sequence in every role)
-    const int esub = (warp - 2) >> 2;                // epilogue: A tile of this warp
+    const int eidx = (warp - 2) >> 2;               // epilogue: (A tile, column part) of this warp
+    const int esub = eidx % MT, ecol = eidx / MT;
     const int erow = kM * esub + 32 * (warp & 3) + lane;   // query row; TMEM lane = erow % 128
     for (uint32_t w0 = nb0; w0 < nb1; w0 += kMaxWin) {
         const int nwin = (int)min((uint32_t)kMaxWin, nb1 - w0);
@@ -229,6 +247,10 @@ __global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_u
                     for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
                         const uint32_t st = c % ST, ph = (c / ST) & 1u;
                         umma::mbar_wait(&S.empty[st], ph ^ 1u);
+                        if (P.debug & 2) {   // timing experiment: no candidate loads
+                            umma::mbar_arrive(&S.full[st]);
+                            continue;
+                        }
                         umma::mbar_arrive_expect_tx(&S.full[st], kBlockBytes);
                         umma::bulk_g2s(umma::smem_u32(S.b[st]), P.pts16 + (size_t)(rb + bi * BN) * KP, kBlockBytes,
                                        &S.full[st]);
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_u
                     }
                 }
             }
-        } else if (esub < nsub) {   // ---------------- epilogue (warps 2 .. 2 + 4 nsub - 1)
+        } else if (esub < nsub) {   // ---------------- epilogue
             uint32_t c = cnt;
             const uint32_t qpos = q0 + erow;
             const bool rvalid = erow < (int)nq;
@@ -280,30 +302,51 @@ __global__ void __launch_bounds__(32 * ws_warps<MT>(), MT == 1 ? 2 : 1) k_join_u
                     const uint32_t ab = c % NACC, aph = (c / NACC) & 1u;
                     umma::mbar_wait(&S.accf[ab], aph);
                     umma::fence_after();
-                    // all BN columns in flight at once, one wait, then release the accumulator
-                    uint32_t v[NL][32];
-                    const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN);
-#pragma unroll
-                    for (int x = 0; x < NL; ++x) umma::tmem_ld32_nowait(tcol + 32 * x, v[x]);
-                    umma::tmem_wait_ld();
-                    umma::fence_before();
-                    __syncwarp();
-                    if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
-                    uint32_t all = 0xffffffffu;
-#pragma unroll
-                    for (int x = 0; x < NL; ++x)
-#pragma unroll
-                        for (int y = 0; y < 32; ++y) all &= v[x][y];
+                    const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN + ecol * CW);
+                    if (P.debug & 1) {   // timing experiment: no accumulator reads
+                        __syncwarp();
+                        if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                        continue;
+                    }
+                    // CW columns in chunks of <= 64 (two loads in flight, one wait); the
+                    // accumulator is released right after the last wait.  Survivors:
+                    // mask bit j of word h = column 64 h + j.
                     unsigned long long mask[2] = {0, 0};
-                    if (rvalid && !(all >> 31)) {   // rare: some accumulator > +0
 #pragma unroll
-                        for (int x = 0; x < NL; ++x)
+                    for (int h = 0; h < (NL + 1) / 2; ++h) {
+                        constexpr int NC = NL < 2 ? NL : 2;
+                        uint32_t v[NC][32];
 #pragma unroll
-                            for (int y = 0; y < 32; ++y)
-                                if (!(v[x][y] >> 31)) mask[x >> 1] |= 1ull << (32 * (x & 1) + y);
+                        for (int x = 0; x < NC; ++x) umma::tmem_ld32_nowait(tcol + 64 * h + 32 * x, v[x]);
+                        umma::tmem_wait_ld();
+                        if (h == (NL + 1) / 2 - 1) {
+                            umma::fence_before();
+                            __syncwarp();
+                            if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                        }
+                        if (P.debug & 4) continue;   // timing experiment: reads only
+                        // sign bits: balanced AND tree (short dependency chains)
+                        uint32_t t[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const int e0 = (4 * k) % (32 * NC);
+                            t[k] = v[e0 / 32][e0 % 32] & v[(e0 + 1) / 32][(e0 + 1) % 32] &
+                                   v[(e0 + 2) / 32][(e0 + 2) % 32] & v[(e0 + 3) / 32][(e0 + 3) % 32];
+                        }
+#pragma unroll
+                        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                            for (int k = 0; k < w; ++k) t[k] &= t[k + w];
+                        if (rvalid && !(t[0] >> 31)) {   // rare: some accumulator > +0
+#pragma unroll
+                            for (int x = 0; x < NC; ++x)
+#pragma unroll
+                                for (int y = 0; y < 32; ++y)
+                                    if (!(v[x][y] >> 31)) mask[h] |= 1ull << (32 * x + y);
+                        }
                     }
                     if (!__any_sync(0xffffffffu, (mask[0] | mask[1]) != 0ull)) continue;
-                    const uint32_t base = rb + bi * BN;
+                    const uint32_t base = rb + bi * BN + ecol * CW;
 #pragma unroll
                     for (int hh = 0; hh < (NL + 1) / 2; ++hh) {
                         unsigned long long m = mask[hh];
@@ -406,43 +449,46 @@ __global__ void __launch_bounds__(128) k_umma_selftest(const __half* __restrict_
     if (warp == 0) umma::tmem_dealloc(tmem, kN);
 }
 
-template <int KP, int BN, int MT, int MODE, bool SYM>
+template <int KP, int BN, int MT, int SL, int EPW, int MODE, bool SYM>
 int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
-    // MT = 1: at most two CTAs per SM (their 2 x 256 TMEM columns fill the SM's 512);
-    // MT = 2: exactly one (512 columns), forced by > 114 KB of shared memory
-    const size_t smem = std::max<size_t>(sizeof(WsSmem<KP, BN, MT>), MT == 1 ? 80 * 1024 : 120 * 1024);
-    static_assert(sizeof(WsSmem<KP, BN, MT>) <= 227 * 1024, "shared memory");
+    using Smem = WsSmem<KP, BN, MT, SL, EPW>;
+    // two CTAs per SM (2 x 256 TMEM columns) or exactly one (512 columns),
+    // forced by > 114 KB of shared memory
+    const size_t smem = std::max<size_t>(sizeof(Smem), ws_ctas_per_sm<BN, MT, SL>() == 2 ? 80 * 1024 : 120 * 1024);
+    static_assert(sizeof(Smem) <= 227 * 1024 / ws_ctas_per_sm<BN, MT, SL>() - 1024, "shared memory");
     static bool attr_done = false;
     if (!attr_done) {
-        GJ_CUDA(cudaFuncSetAttribute((const void*)k_join_umma<KP, BN, MT, MODE, SYM>,
+        GJ_CUDA(cudaFuncSetAttribute((const void*)k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_done = true;
     }
-    k_join_umma<KP, BN, MT, MODE, SYM><<<grid_ctas(a, (int)p.tile_q, kM * MT), 32 * ws_warps<MT>(), smem, s>>>(p, a);
+    k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM>
+        <<<grid_ctas(a, (int)p.tile_q, kM * MT), 32 * ws_warps<MT, EPW>(), smem, s>>>(p, a);
     count_launch();
     GJ_CUDA(cudaGetLastError());
     return GJ_OK;
 }
 
-template <int KP, int BN, int MT>
+template <int KP, int BN, int MT, int SL, int EPW>
 int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
-    if (mode == kEmit) return sym ? launch_umma_k<KP, BN, MT, kEmit, true>(p, a, s)
-                                  : launch_umma_k<KP, BN, MT, kEmit, false>(p, a, s);
-    return sym ? launch_umma_k<KP, BN, MT, kCount, true>(p, a, s) : launch_umma_k<KP, BN, MT, kCount, false>(p, a, s);
+    if (mode == kEmit) return sym ? launch_umma_k<KP, BN, MT, SL, EPW, kEmit, true>(p, a, s)
+                                  : launch_umma_k<KP, BN, MT, SL, EPW, kEmit, false>(p, a, s);
+    return sym ? launch_umma_k<KP, BN, MT, SL, EPW, kCount, true>(p, a, s)
+               : launch_umma_k<KP, BN, MT, SL, EPW, kCount, false>(p, a, s);
 }
 
-template <int BN, int MT>
+template <int BN, int MT, int SL, int EPW>
 int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     switch (ix->k16) {
-        case 16: return launch_umma<16, BN, MT>(p, mode, a, sym, s);
-        case 32: return launch_umma<32, BN, MT>(p, mode, a, sym, s);
-        case 48: return launch_umma<48, BN, MT>(p, mode, a, sym, s);
-        case 64: return launch_umma<64, BN, MT>(p, mode, a, sym, s);
-        case 80: return launch_umma<80, BN, MT>(p, mode, a, sym, s);
-        case 96: return launch_umma<96, BN, MT>(p, mode, a, sym, s);
-        case 112: return launch_umma<112, BN, MT>(p, mode, a, sym, s);
-        default: return launch_umma<128, BN, MT>(p, mode, a, sym, s);
+        case 16: return launch_umma<16, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 32: return launch_umma<32, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 48: return launch_umma<48, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 64: return launch_umma<64, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 80: return launch_umma<80, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 96: return launch_umma<96, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 112: return launch_umma<112, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        default: return launch_umma<128, BN, MT, SL, EPW>(p, mode, a, sym, s);
     }
 }
 
@@ -451,11 +497,18 @@ int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const Jo
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     const JoinParams p = join_params(ix);
     const bool sym = ix->opt.symmetric != 0;
-    // block width: 128 candidates (default) or 64 (GJ_UMMA_BN=64); A tiles per CTA = tile_q / 128
-    static const int bn = [] { const char* e = getenv("GJ_UMMA_BN"); return e && atoi(e) == 64 ? 64 : 128; }();
-    const int mt = ix->tile_q / kM;
-    if (mt == 1) return bn == 64 ? launch_umma_kp<64, 1>(ix, p, mode, a, sym, s) : launch_umma_kp<128, 1>(ix, p, mode, a, sym, s);
-    return bn == 64 ? launch_umma_kp<64, 2>(ix, p, mode, a, sym, s) : launch_umma_kp<128, 2>(ix, p, mode, a, sym, s);
+    // A tiles per CTA = tile_q / 128.  MT = 1 (default): 256-candidate blocks
+    // (UMMA N = 256: the issue loop's barrier handshakes are amortised over 384
+    // tensor cycles, tools/micro/umma_issue), one 256-column slot per CTA and
+    // two CTAs per SM (each CTA's epilogue overlaps the other's MMA), 8
+    // epilogue warps per CTA.  Timing comparisons: GJ_UMMA_CFG=2 (128-candidate
+    // blocks, two slots per CTA, two CTAs per SM), GJ_UMMA_CFG=3 (256-candidate
+    // blocks, two slots, one CTA per SM with 16 epilogue warps).
+    static const int cfg = [] { const char* e = getenv("GJ_UMMA_CFG"); return e ? atoi(e) : 0; }();
+    if (ix->tile_q / kM == 2) return launch_umma_kp<128, 2, 2, 1>(ix, p, mode, a, sym, s);
+    if (cfg == 2) return launch_umma_kp<128, 1, 2, 2>(ix, p, mode, a, sym, s);
+    if (cfg == 3) return launch_umma_kp<256, 1, 2, 4>(ix, p, mode, a, sym, s);
+    return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
 }
 
 int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s) {
