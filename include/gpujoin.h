@@ -72,8 +72,9 @@ typedef struct {
                             gj_join_stats always runs the FP64 scan.                          */
     int32_t mma_tiles;   /* filter 2 only: 128-query accumulator tiles per tcgen05 CTA that
                             share every staged candidate block (UMMA M = 128 each):
-                            2 = query tiles of 256 points, one CTA per SM, half the candidate
-                            traffic per test (default); 1 = tiles of 128, two CTAs per SM;
+                            1 = query tiles of 128 points, 256-candidate blocks, two CTAs
+                            per SM (default); 2 = tiles of 256 points, 128-candidate blocks,
+                            one CTA per SM, half the candidate traffic per test;
                             0 = default.  The pair set does not depend on it.               */
 } gj_options;
 

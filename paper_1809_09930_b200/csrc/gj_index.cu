@@ -586,8 +586,8 @@ int build_index(Index* ix, const double* X) {
     k_adjacent<true><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, nullptr,
                                                             nullptr, nullptr, ix->nbr_off, ix->nbr, ix->nbr_self); count_launch();
     GJ_CUDA(cudaGetLastError());
-    // 8. tiles, heaviest first (256 queries for the two-accumulator tcgen05 kernel)
-    ix->tile_q = ix->filter == 2 ? 128 * (ix->opt.mma_tiles == 1 ? 1 : 2) : kTileQ;
+    // 8. tiles, heaviest first (256 queries for the two-accumulator-tile tcgen05 kernel)
+    ix->tile_q = ix->filter == 2 ? 128 * (ix->opt.mma_tiles == 2 ? 2 : 1) : kTileQ;
     k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, (uint32_t)ix->tile_q, pos); count_launch();
     if ((rc = scan_u32(pos, pos, G, d_tot, s))) return rc;
     GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
