@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--batch-size", type=int, default=100_000_000)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-stats", action="store_true",
+                   help="skip the FP64 work-counter pass (roofline = null); for large sweep workloads")
     p.add_argument("--cpu-sample", type=int, default=24, help="oracle query sample for cpu_baseline")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu baseline/clocks")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo lets several ranks share one GPU "
@@ -258,7 +260,7 @@ def main():
     ix0 = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
     info = ix0.info()
     exact = ix0.estimate(1.0, rank, world)
-    stats = ix0.stats(rank, world) if not args.profile else None
+    stats = ix0.stats(rank, world) if not (args.profile or args.no_stats) else None
     ix0.free()
     cap = int(exact * 1.02) + 65536
     out = torch.empty((cap, 2), dtype=torch.int32, device=dev)
