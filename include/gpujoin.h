@@ -213,6 +213,12 @@ GJ_API void gj_free_index(gj_index* idx);
 GJ_API const char* gj_last_error(void);
 GJ_API int32_t gj_abi_version(void);
 /* Number of CUDA kernels this library has launched in this process. */
+/* Device memory of every index and join comes from a library-private, stream-ordered
+ * memory pool per device that keeps freed memory cached for the next build / join
+ * (no driver remapping per step).  This returns the cached, unused part to the driver;
+ * it synchronises the current device.  GJ_OK, or GJ_ERR_CUDA. */
+GJ_API int gj_release_cached_memory(void);
+
 GJ_API int64_t gj_launch_count(void);
 
 #ifdef __cplusplus

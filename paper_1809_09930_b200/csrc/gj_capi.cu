@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <string>
 
 #include "gj_internal.cuh"
@@ -19,6 +20,45 @@ namespace gj {
 static thread_local std::string g_err;
 std::atomic<long long> g_launches{0};
 void set_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+cudaMemPool_t g_pool[64] = {};
+std::mutex g_pool_mu;
+cudaError_t device_pool(cudaMemPool_t* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if ((e = cudaMemPoolCreate(&g_pool[dev], &props)) != cudaSuccess) return e;
+        uint64_t keep = ~0ull;
+        if ((e = cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+    }
+    *out = g_pool[dev];
+    return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t pool_malloc_raw(void** p, size_t bytes, cudaStream_t s) {
+    cudaMemPool_t pool;
+    cudaError_t e = device_pool(&pool);
+    if (e != cudaSuccess) return e;
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+cudaError_t pool_trim() {
+    cudaMemPool_t pool;
+    cudaError_t e = device_pool(&pool);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+    return cudaMemPoolTrimTo(pool, 0);
+}
 
 namespace {
 
@@ -95,6 +135,11 @@ int32_t gj_abi_version(void) { return 3; }
 
 int64_t gj_launch_count(void) { return (int64_t)g_launches.load(); }
 
+int gj_release_cached_memory(void) {
+    GJ_CUDA(pool_trim());
+    return GJ_OK;
+}
+
 const char* gj_last_error(void) { return g_err.c_str(); }
 
 void gj_default_options(gj_options* opt) {
@@ -139,7 +184,7 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     int rc = GJ_OK;
     if (!is_device_ptr(points)) {
         size_t bytes = (size_t)n_points * dim * sizeof(double);
-        if (cudaMallocAsync(&staged, bytes, ix.stream) != cudaSuccess) {
+        if (pool_malloc(&staged, bytes, ix.stream) != cudaSuccess) {
             cudaGetLastError();
             set_error("device allocation for staged points failed");
             delete h;
@@ -325,10 +370,11 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
     bool overflow = false;
     auto cleanup = [&]() {
         for (int i = 0; i < 3; ++i) {
-            if (dbuf[i]) cudaFree(dbuf[i]);
+            if (dbuf[i]) cudaFreeAsync(dbuf[i], ix.stream);
             if (hbuf[i]) cudaFreeHost(hbuf[i]);
         }
-        if (dcnt) cudaFree(dcnt);
+        if (dcnt) cudaFreeAsync(dcnt, ix.stream);
+        cudaStreamSynchronize(ix.stream);
         if (hcnt) cudaFreeHost(hcnt);
     };
     for (int i = 0; i < 3; ++i) {
@@ -336,7 +382,7 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
             GJ_CUDA(cudaStreamCreateWithFlags(&ix.pipe_stream[i], cudaStreamNonBlocking));
             GJ_CUDA(cudaEventCreateWithFlags(&ix.pipe_event[i], cudaEventDisableTiming));
         }
-        if (cudaMalloc(&dbuf[i], (size_t)per * 2 * sizeof(uint32_t)) != cudaSuccess ||
+        if (pool_malloc(&dbuf[i], (size_t)per * 2 * sizeof(uint32_t), ix.stream) != cudaSuccess ||
             (!direct && cudaMallocHost(&hbuf[i], (size_t)per * 2 * sizeof(uint32_t)) != cudaSuccess)) {
             cudaGetLastError();
             cleanup();
@@ -344,7 +390,7 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
             return GJ_ERR_NOMEM;
         }
     }
-    if (cudaMalloc(&dcnt, 3 * sizeof(uint64_t)) != cudaSuccess || cudaMallocHost(&hcnt, 3 * sizeof(uint64_t)) != cudaSuccess) {
+    if (pool_malloc(&dcnt, 3 * sizeof(uint64_t), ix.stream) != cudaSuccess || cudaMallocHost(&hcnt, 3 * sizeof(uint64_t)) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
         set_error("counter allocation failed");
@@ -385,9 +431,9 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
             if ((int64_t)hcnt[i] <= per) break;
             // re-plan: grow this slot's buffers and rerun the batch (§3.2.2 estimate was low)
             per = (int64_t)hcnt[i] + 1024;
-            cudaFree(dbuf[i]);
+            cudaFreeAsync(dbuf[i], st);
             dbuf[i] = nullptr;
-            if (cudaMalloc(&dbuf[i], (size_t)per * 2 * sizeof(uint32_t)) != cudaSuccess) { cudaGetLastError(); rc = GJ_ERR_NOMEM; break; }
+            if (pool_malloc(&dbuf[i], (size_t)per * 2 * sizeof(uint32_t), st) != cudaSuccess) { cudaGetLastError(); rc = GJ_ERR_NOMEM; break; }
             if (!direct) {
                 cudaFreeHost(hbuf[i]);
                 hbuf[i] = nullptr;
@@ -447,8 +493,8 @@ int gj_neighbor_table(gj_index* h, uint32_t* pairs, int64_t n_pairs, uint64_t* o
     uint64_t* keys = nullptr;
     uint32_t* vals = nullptr;
     const int64_t n = std::max<int64_t>(n_pairs, 1);
-    GJ_CUDA(cudaMallocAsync(&keys, n * sizeof(uint64_t), s));
-    GJ_CUDA(cudaMallocAsync(&vals, n * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&keys, n * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&vals, n * sizeof(uint32_t), s));
     unsigned blocks = (unsigned)((n + 255) / 256);
     if (n_pairs > 0) {
         k_pairs_to_keys<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint2*>(pairs), n_pairs, keys); count_launch();
@@ -469,11 +515,11 @@ int gj_neighbor_table(gj_index* h, uint32_t* pairs, int64_t n_pairs, uint64_t* o
 void gj_free_index(gj_index* h) {
     if (!h) return;
     Index& ix = h->ix;
-    cudaStreamSynchronize(ix.stream);
     void* ptrs[] = {ix.pts, ix.pts32, ix.pts16, ix.norm16, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
                     ix.tile_order, ix.tile_work, ix.meta, ix.scratch_count};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    for (void* p : ptrs)   // back to the library pool (stream-ordered)
+        if (p) cudaFreeAsync(p, ix.stream);
+    cudaStreamSynchronize(ix.stream);
     for (int i = 0; i < 3; ++i) {
         if (ix.pipe_stream[i]) cudaStreamDestroy(ix.pipe_stream[i]);
         if (ix.pipe_event[i]) cudaEventDestroy(ix.pipe_event[i]);

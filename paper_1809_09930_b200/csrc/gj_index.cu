@@ -323,7 +323,7 @@ int col_reduce(const double* X, int64_t m, int64_t rstride, int n, int mode, con
     int64_t need = (m + rpb - 1) / rpb;
     int nb = (int)std::max<int64_t>(1, std::min<int64_t>(need, 592));
     double* part = nullptr;
-    GJ_CUDA(cudaMallocAsync(&part, 2 * (size_t)nb * n * sizeof(double), s));
+    GJ_CUDA(pool_malloc(&part, 2 * (size_t)nb * n * sizeof(double), s));
     k_col_reduce<<<nb, bs, 2 * bs * sizeof(double), s>>>(X, m, rstride, n, mode, mean, part, part + (size_t)nb * n); count_launch();
     k_col_final<<<(n + 127) / 128, 128, 0, s>>>(part, part + (size_t)nb * n, nb, n, mode, m, outa, outb); count_launch();
     GJ_CUDA(cudaGetLastError());
@@ -460,11 +460,11 @@ static int make_fp16(Index* ix, bool* ok) {
     // rows padded to a multiple of 8 plus one 256-row block of zeros: block loads
     // (<= 256 rows) that start at a row multiple of 8 never read past the allocation
     const size_t rows16 = (size_t)((N + 7) & ~7ll) + 256;
-    GJ_CUDA(cudaMallocAsync(&ix->pts16, rows16 * ix->k16 * sizeof(__half), s));
+    GJ_CUDA(pool_malloc(&ix->pts16, rows16 * ix->k16 * sizeof(__half), s));
     GJ_CUDA(cudaMemsetAsync(ix->pts16, 0, rows16 * ix->k16 * sizeof(__half), s));
-    GJ_CUDA(cudaMallocAsync(&ix->norm16, (size_t)N * sizeof(double), s));
+    GJ_CUDA(pool_malloc(&ix->norm16, (size_t)N * sizeof(double), s));
     unsigned long long* d_r2 = nullptr;
-    GJ_CUDA(cudaMallocAsync(&d_r2, sizeof(*d_r2), s));
+    GJ_CUDA(pool_malloc(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
     k_make16<<<blocks_for(N * ix->k16, 256), 256, 0, s>>>(ix->pts, N, ix->n, ix->n_pad, ix->k16, ix->tc_scale,
                                                           ix->meta, ix->pts16); count_launch();
@@ -497,7 +497,7 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaEventCreate(&ev1));
     GJ_CUDA(cudaEventRecord(ev0, s));
 
-    GJ_CUDA(cudaMallocAsync(&ix->meta, sizeof(Meta), s));
+    GJ_CUDA(pool_malloc(&ix->meta, sizeof(Meta), s));
     GJ_CUDA(cudaMemsetAsync(ix->meta, 0, sizeof(Meta), s));
     Meta* M = ix->meta;
     // 1. min/max over D, variance over the sample
@@ -505,7 +505,7 @@ int build_index(Index* ix, const double* X) {
     const int64_t step = std::max<int64_t>(1, (int64_t)llround(1.0 / ix->opt.sample_frac));
     const int64_t m = (N + step - 1) / step;
     double* mean = nullptr;
-    GJ_CUDA(cudaMallocAsync(&mean, n * sizeof(double), s));
+    GJ_CUDA(pool_malloc(&mean, n * sizeof(double), s));
     if ((rc = col_reduce(X, m, step, n, kSum, nullptr, mean, nullptr, s))) return rc;
     if ((rc = col_reduce(X, m, step, n, kSqDev, mean, M->var, nullptr, s))) return rc;
     GJ_CUDA(cudaFreeAsync(mean, s));
@@ -523,10 +523,10 @@ int build_index(Index* ix, const double* X) {
     // 3. keys
     uint64_t *cellkey = nullptr, *ukey = nullptr, *tmp64 = nullptr;
     uint32_t* idx = nullptr;
-    GJ_CUDA(cudaMallocAsync(&cellkey, N * sizeof(uint64_t), s));
-    GJ_CUDA(cudaMallocAsync(&ukey, N * sizeof(uint64_t), s));
-    GJ_CUDA(cudaMallocAsync(&tmp64, N * sizeof(uint64_t), s));
-    GJ_CUDA(cudaMallocAsync(&idx, N * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&cellkey, N * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&ukey, N * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&tmp64, N * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&idx, N * sizeof(uint32_t), s));
     k_cell_keys<<<blocks_for(N, 256), 256, 0, s>>>(X, N, n, k, ix->u, ix->eps, M, cellkey, ukey, idx); count_launch();
     GJ_CUDA(cudaGetLastError());
     // 4. stable sort by u, then by cell id
@@ -540,9 +540,9 @@ int build_index(Index* ix, const double* X) {
     if ((rc = varying_bits_u64(tmp64, N, &vb, s))) return rc;
     if ((rc = radix_sort_u64(tmp64, idx, N, vb, s))) return rc;
     // 5. sorted, reordered point array
-    GJ_CUDA(cudaMallocAsync(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
-    GJ_CUDA(cudaMallocAsync(&ix->orig, N * sizeof(uint32_t), s));
-    if (want32) GJ_CUDA(cudaMallocAsync(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
+    GJ_CUDA(pool_malloc(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
+    GJ_CUDA(pool_malloc(&ix->orig, N * sizeof(uint32_t), s));
+    if (want32) GJ_CUDA(pool_malloc(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
     k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, ix->pts32); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     if (ix->filter >= 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
@@ -554,9 +554,9 @@ int build_index(Index* ix, const double* X) {
     }
     // 6. non-empty cells
     uint32_t *head = nullptr, *pos = nullptr, *d_tot = nullptr;
-    GJ_CUDA(cudaMallocAsync(&head, N * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&pos, N * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&d_tot, 4 * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&head, N * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&pos, N * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&d_tot, 4 * sizeof(uint32_t), s));
     k_heads<<<blocks_for(N, 256), 256, 0, s>>>(tmp64, N, head); count_launch();
     if ((rc = scan_u32(head, pos, N, d_tot, s))) return rc;
     uint32_t h_tot = 0;
@@ -564,16 +564,16 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaStreamSynchronize(s));
     const int64_t G = h_tot;
     ix->G = G;
-    GJ_CUDA(cudaMallocAsync(&ix->cell_id, G * sizeof(uint64_t), s));
-    GJ_CUDA(cudaMallocAsync(&ix->cell_start, (G + 1) * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->cell_id, G * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&ix->cell_start, (G + 1) * sizeof(uint32_t), s));
     k_cells<<<blocks_for(N, 256), 256, 0, s>>>(tmp64, head, pos, N, ix->cell_id, ix->cell_start, G); count_launch();
     GJ_CUDA(cudaGetLastError());
     // 7. adjacent non-empty cells
     uint32_t* cnt = head;               // reuse (G <= N)
     uint64_t* cand = tmp64;             // reuse: tmp64 no longer needed
     uint64_t* cand_after = cellkey;     // reuse: cell keys no longer needed
-    GJ_CUDA(cudaMallocAsync(&ix->nbr_off, (G + 1) * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&ix->nbr_self, G * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->nbr_off, (G + 1) * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->nbr_self, G * sizeof(uint32_t), s));
     k_adjacent<false><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, cnt, cand,
                                                              cand_after, nullptr, nullptr, nullptr); count_launch();
     GJ_CUDA(cudaGetLastError());
@@ -582,7 +582,7 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     GJ_CUDA(cudaStreamSynchronize(s));
     ix->A = h_tot;
-    GJ_CUDA(cudaMallocAsync(&ix->nbr, std::max<int64_t>(1, ix->A) * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->nbr, std::max<int64_t>(1, ix->A) * sizeof(uint32_t), s));
     k_adjacent<true><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, nullptr,
                                                             nullptr, nullptr, ix->nbr_off, ix->nbr, ix->nbr_self); count_launch();
     GJ_CUDA(cudaGetLastError());
@@ -594,13 +594,13 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaStreamSynchronize(s));
     const int64_t T = h_tot;
     ix->T = T;
-    GJ_CUDA(cudaMallocAsync(&ix->tile_cell, T * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&ix->tile_q0, T * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&ix->tile_order, T * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&ix->tile_work, T * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&ix->tile_cell, T * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->tile_q0, T * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->tile_order, T * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&ix->tile_work, T * sizeof(uint64_t), s));
     uint64_t* skey = ukey;              // reuse (T <= N)
     unsigned long long* d_total = nullptr;
-    GJ_CUDA(cudaMallocAsync(&d_total, sizeof(*d_total), s));
+    GJ_CUDA(pool_malloc(&d_total, sizeof(*d_total), s));
     GJ_CUDA(cudaMemsetAsync(d_total, 0, sizeof(*d_total), s));
     k_tile_fill<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, pos, cand, cand_after, ix->opt.symmetric, G,
                                                    (uint32_t)ix->tile_q,
@@ -611,7 +611,7 @@ int build_index(Index* ix, const double* X) {
     if ((rc = radix_sort_u64(skey, ix->tile_order, T, vb, s))) return rc;
     unsigned long long h_total = 0;
     GJ_CUDA(cudaMemcpyAsync(&h_total, d_total, sizeof(h_total), cudaMemcpyDeviceToHost, s));
-    GJ_CUDA(cudaMallocAsync(&ix->scratch_count, 8 * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&ix->scratch_count, 8 * sizeof(uint64_t), s));
     GJ_CUDA(cudaFreeAsync(d_total, s));
     GJ_CUDA(cudaFreeAsync(cellkey, s));
     GJ_CUDA(cudaFreeAsync(ukey, s));

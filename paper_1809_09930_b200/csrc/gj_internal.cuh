@@ -16,6 +16,18 @@ constexpr int kMaxDim = 128;         // largest supported n (query dims live in 
 
 void set_error(const std::string& msg);
 
+// Device memory: every allocation of the library comes from one private
+// stream-ordered pool per device whose release threshold is unbounded, so
+// memory freed by one join (index arrays, result batches) is reused by the
+// next without returning to the driver (no page-table remapping per step).
+// gj_release_cached_memory() trims it.
+cudaError_t pool_malloc_raw(void** p, size_t bytes, cudaStream_t s);
+template <typename T>
+inline cudaError_t pool_malloc(T** p, size_t bytes, cudaStream_t s) {
+    return pool_malloc_raw(reinterpret_cast<void**>(p), bytes, s);
+}
+cudaError_t pool_trim();
+
 // Kernels launched by this library (bench.py reports it as gpu_launches).
 extern std::atomic<long long> g_launches;
 inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }

@@ -198,7 +198,7 @@ int scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* d_total, cu
     }
     int64_t nb = (n + kScanTile - 1) / kScanTile;
     uint32_t* sums = nullptr;
-    GJ_CUDA(cudaMallocAsync(&sums, nb * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&sums, nb * sizeof(uint32_t), s));
     k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, sums); count_launch();
     k_scan_sums<<<1, 1024, 0, s>>>(sums, nb, d_total); count_launch();
     k_scan_down<<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, sums); count_launch();
@@ -211,7 +211,7 @@ int varying_bits_u64(const uint64_t* keys, int64_t n, uint64_t* h_out, cudaStrea
     *h_out = 0;
     if (n <= 1) return GJ_OK;
     unsigned long long* d = nullptr;
-    GJ_CUDA(cudaMallocAsync(&d, sizeof(*d), s));
+    GJ_CUDA(pool_malloc(&d, sizeof(*d), s));
     GJ_CUDA(cudaMemsetAsync(d, 0, sizeof(*d), s));
     int blocks = (int)std::min<int64_t>(1184, (n + 255) / 256);
     k_or_xor<<<blocks, 256, 0, s>>>(keys, n, d); count_launch();
@@ -227,9 +227,9 @@ int radix_sort_u64(uint64_t* keys, uint32_t* vals, int64_t n, uint64_t bits_mask
     const int64_t nb = (n + kTile - 1) / kTile;
     uint64_t* k2 = nullptr;
     uint32_t *v2 = nullptr, *hist = nullptr;
-    GJ_CUDA(cudaMallocAsync(&k2, n * sizeof(uint64_t), s));
-    GJ_CUDA(cudaMallocAsync(&v2, n * sizeof(uint32_t), s));
-    GJ_CUDA(cudaMallocAsync(&hist, 256 * nb * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&k2, n * sizeof(uint64_t), s));
+    GJ_CUDA(pool_malloc(&v2, n * sizeof(uint32_t), s));
+    GJ_CUDA(pool_malloc(&hist, 256 * nb * sizeof(uint32_t), s));
     uint64_t *ka = keys, *kb = k2;
     uint32_t *va = vals, *vb = v2;
     int rc = GJ_OK;

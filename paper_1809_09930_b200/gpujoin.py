@@ -21,7 +21,7 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
            "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_tc_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
            "gj_self_join_host", "gj_join_stats", "gj_neighbor_table", "gj_free_index", "gj_last_error",
-           "gj_abi_version", "gj_launch_count"]
+           "gj_abi_version", "gj_launch_count", "gj_release_cached_memory"]
 
 
 class Options(C.Structure):
@@ -83,6 +83,7 @@ def lib():
         "gj_last_error": (C.c_char_p, []),
         "gj_abi_version": (C.c_int32, []),
         "gj_launch_count": (C.c_int64, []),
+        "gj_release_cached_memory": (C.c_int, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -268,6 +269,11 @@ def selftest_umma(A, B, D, stream=0):
 def launch_count() -> int:
     """Kernels launched by libgpujoin in this process so far."""
     return int(lib().gj_launch_count())
+
+
+def release_cached_memory() -> None:
+    """Return the library pool's cached device memory to the driver (gj_release_cached_memory)."""
+    _check(lib().gj_release_cached_memory())
 
 
 def abi_version() -> int:
