@@ -260,7 +260,12 @@ def main():
     ix0 = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
     info = ix0.info()
     exact = ix0.estimate(1.0, rank, world)
-    stats = ix0.stats(rank, world) if not (args.profile or args.no_stats) else None
+    # work counters for the roofline: the tensor-core filters' unit is the
+    # evaluated test (gj_join_counts, no distance work); the SHORTC scans need the
+    # per-dimension counts of the FP64 stats scan (gj_join_stats)
+    stats = None
+    if not (args.profile or args.no_stats):
+        stats = ix0.counts(rank, world) if info.filter in (2, 3) else ix0.stats(rank, world)
     ix0.free()
     cap = int(exact * 1.02) + 65536
     out = torch.empty((cap, 2), dtype=torch.int32, device=dev)
@@ -385,8 +390,8 @@ def main():
         achieved = alg * scale / (jms / 1000.0) / 1e12
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kern, "peak_note": pnote,
-                "alg": {"tests_evaluated": stats["tests_evaluated"], "dims_evaluated": stats["dims_evaluated"],
-                        "paper_tests": stats["tests"], "paper_dims": stats["dims"], "cells": stats["cells"],
+                "alg": {"tests_evaluated": stats["tests_evaluated"], "dims_evaluated": stats.get("dims_evaluated"),
+                        "paper_tests": stats["tests"], "paper_dims": stats.get("dims"), "cells": stats["cells"],
                         "alg_tflop_per_join": alg * scale / 1e12},
                 "join_ms": jms, "join_share_of_step": jms / ms,
                 "filter_margin": info.filter_margin}

@@ -200,6 +200,14 @@ GJ_API int gj_self_join(gj_index* idx, uint32_t* out_pairs, int64_t capacity, in
 GJ_API int gj_self_join_host(gj_index* idx, uint32_t* out_pairs, int64_t capacity, int32_t rank,
                       int32_t world, int64_t batch_size, int64_t* n_pairs, int32_t* n_batches_out);
 
+/* The work counters cells, tests and tests_evaluated of gj_join_stats (same
+ * definitions, equal values) for the tiles of (rank, world), WITHOUT the
+ * distance work: per query and adjacent cell the SORTIDU window is found by
+ * binary search (§4.3).  dims, pairs and dims_evaluated are set to -1.
+ * Cheap (milliseconds at |D| = 2e6): the roofline denominator of the
+ * tensor-core filters, whose unit of work is the evaluated test. */
+GJ_API int gj_join_counts(gj_index* idx, int32_t rank, int32_t world, gj_stats* st);
+
 /* Work counters of rank's share (cells visited, SORTIDU-window tests,
  * algorithmic SHORTC dims, pairs).  Synchronous; slower than the join. */
 GJ_API int gj_join_stats(gj_index* idx, int32_t rank, int32_t world, gj_stats* st);

@@ -2,6 +2,7 @@
 // the Fig. 4 result pipeline.  All arithmetic of the method runs in the
 // kernels of gj_index.cu / gj_join.cu / gj_radix.cu.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -358,8 +359,12 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
     if (int rc = gj_estimate(h, 0.01, rank, world, &est)) return rc;
     const int64_t nb = gj_num_batches(est, batch_size);
     if (n_batches_out) *n_batches_out = (int32_t)nb;
-    // per-stream device buffers sized for one batch (+25% headroom over the estimate)
-    int64_t per = std::max<int64_t>(1024, (int64_t)(1.25 * (double)est / (double)nb) + 1024);
+    // per-stream device buffers sized for one batch (+25% headroom over the estimate);
+    // a slot whose batch overflows is regrown on its own (cap_of[i])
+    // (GJ_BATCH_HEADROOM overrides the 1.25 factor: tests force the regrow path with it)
+    static const double headroom = [] { const char* e = getenv("GJ_BATCH_HEADROOM"); return e ? atof(e) : 1.25; }();
+    const int64_t per = std::max<int64_t>(1024, (int64_t)(headroom * (double)est / (double)nb) + 1024);
+    int64_t cap_of[3] = {per, per, per};
     const bool direct = out_pairs && is_pinned_host(out_pairs);
     uint32_t* dbuf[3] = {nullptr, nullptr, nullptr};
     uint32_t* hbuf[3] = {nullptr, nullptr, nullptr};
@@ -422,22 +427,22 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
             GJ_CUDA(cudaMemsetAsync(dcnt + i, 0, sizeof(uint64_t), st));
             JoinArgs a{};
             a.out = dbuf[i];
-            a.cap = (uint64_t)per;
+            a.cap = (uint64_t)cap_of[i];
             a.count = dcnt + i;
             batch_tiles(&ix, (int32_t)b, (int32_t)nb, rank, world, &a);
             if ((rc = launch_join(&ix, kEmit, a, st))) break;
             GJ_CUDA(cudaMemcpyAsync(hcnt + i, dcnt + i, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
             GJ_CUDA(cudaStreamSynchronize(st));
-            if ((int64_t)hcnt[i] <= per) break;
+            if ((int64_t)hcnt[i] <= cap_of[i]) break;
             // re-plan: grow this slot's buffers and rerun the batch (§3.2.2 estimate was low)
-            per = (int64_t)hcnt[i] + 1024;
+            cap_of[i] = (int64_t)hcnt[i] + 1024;
             cudaFreeAsync(dbuf[i], st);
             dbuf[i] = nullptr;
-            if (pool_malloc(&dbuf[i], (size_t)per * 2 * sizeof(uint32_t), st) != cudaSuccess) { cudaGetLastError(); rc = GJ_ERR_NOMEM; break; }
+            if (pool_malloc(&dbuf[i], (size_t)cap_of[i] * 2 * sizeof(uint32_t), st) != cudaSuccess) { cudaGetLastError(); rc = GJ_ERR_NOMEM; break; }
             if (!direct) {
                 cudaFreeHost(hbuf[i]);
                 hbuf[i] = nullptr;
-                if (cudaMallocHost(&hbuf[i], (size_t)per * 2 * sizeof(uint32_t)) != cudaSuccess) { cudaGetLastError(); rc = GJ_ERR_NOMEM; break; }
+                if (cudaMallocHost(&hbuf[i], (size_t)cap_of[i] * 2 * sizeof(uint32_t)) != cudaSuccess) { cudaGetLastError(); rc = GJ_ERR_NOMEM; break; }
             }
         }
         if (rc) break;
@@ -462,6 +467,24 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
         set_error("host result buffer too small");
         return GJ_ERR_CAPACITY;
     }
+    return GJ_OK;
+}
+
+int gj_join_counts(gj_index* h, int32_t rank, int32_t world, gj_stats* st) {
+    if (!h || !st) { set_error("null argument"); return GJ_ERR_INVALID; }
+    if (int rc = check_rank(rank, world)) return rc;
+    Index& ix = h->ix;
+    JoinArgs a{};
+    batch_tiles(&ix, 0, 1, rank, world, &a);
+    GJ_CUDA(cudaMemsetAsync(ix.scratch_count, 0, 8 * sizeof(uint64_t), ix.stream));
+    if (int rc = count_tests(&ix, a, (unsigned long long*)ix.scratch_count, ix.stream)) return rc;
+    uint64_t c[3];
+    GJ_CUDA(cudaMemcpyAsync(c, ix.scratch_count, sizeof(c), cudaMemcpyDeviceToHost, ix.stream));
+    GJ_CUDA(cudaStreamSynchronize(ix.stream));
+    st->cells = (int64_t)c[0];
+    st->tests = (int64_t)c[1];
+    st->tests_evaluated = (int64_t)c[2];
+    st->dims = st->pairs = st->dims_evaluated = -1;
     return GJ_OK;
 }
 

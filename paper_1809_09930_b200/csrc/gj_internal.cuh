@@ -199,6 +199,8 @@ __device__ __forceinline__ void query_aug(double T, double nq, bool valid, __hal
     rlo = __double2half(r - (double)__half2float(rhi));
 }
 int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+// cells / paper tests / tests evaluated of the tiles in a (no distance work); adds to d_out[0..2].
+int count_tests(const Index* ix, const JoinArgs& a, unsigned long long* d_out, cudaStream_t s);
 // FP32-prefilter variant (gj_join32.cu); kEmit / kCount only.
 int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // Tensor-core bound variants; kEmit / kCount only.

@@ -255,6 +255,54 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     }
 }
 
+// Work counters without the distance work (gj_join_counts): per query and
+// adjacent cell, the paper's SORTIDU window [lo, hi) by binary search on the
+// u-sorted run (the same predicates as the stats scan: q(u) - c(u) <= eps and
+// not c(u) - q(u) > eps), the own cell restricted to candidates after the query
+// when symmetric.  Counters: [0] cells, [1] paper tests, [2] tests evaluated.
+__global__ void __launch_bounds__(kTileQ) k_count_tests(Params P, JoinArgs A, int sym, unsigned long long* out) {
+    const CtaTile ct = cta_tile(P, A, kTileQ);
+    const int tid = threadIdx.x;
+    unsigned long long cells = 0, tests = 0, evald = 0;
+    if (tid < (int)ct.nq) {
+        const uint32_t g = ct.g, qpos = ct.q0 + tid;
+        const int n_pad = P.n_pad;
+        const double eps = P.eps;
+        const double qu = P.pts[(size_t)qpos * n_pad + P.u];
+        const uint32_t a0 = P.nbr_off[g], a1 = P.nbr_off[g + 1], self = P.nbr_self[g];
+        cells = a1 - a0;
+        for (uint32_t b = sym ? self : a0; b < a1; ++b) {
+            const uint32_t B = P.nbr[b];
+            uint32_t lo = P.cell_start[B], hi = P.cell_start[B + 1];
+            if (P.sortidu) {
+                uint32_t l = lo, h = hi;
+                while (l < h) {   // first c with q(u) - c(u) <= eps
+                    const uint32_t m = (l + h) >> 1;
+                    if (qu - P.pts[(size_t)m * n_pad + P.u] <= eps) h = m; else l = m + 1;
+                }
+                const uint32_t lo2 = l;
+                h = hi;
+                while (l < h) {   // first c with c(u) - q(u) > eps
+                    const uint32_t m = (l + h) >> 1;
+                    if (P.pts[(size_t)m * n_pad + P.u] - qu > eps) h = m; else l = m + 1;
+                }
+                lo = lo2;
+                hi = l;
+            }
+            if (sym && B == g) lo = max(lo, qpos + 1);
+            if (hi > lo) evald += hi - lo;
+        }
+        tests = sym ? 2 * evald + 1 : evald;
+    }
+    unsigned long long v[3] = {cells, tests, evald};
+    for (int i = 0; i < 3; ++i) {
+        unsigned long long x = v[i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((tid & 31) == 0 && x) atomicAdd(out + i, x);
+    }
+}
+
 template <int NPR, bool SYM>
 void launch_mode(const Params& p, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     dim3 grid(grid_ctas(a, (int)p.tile_q, kTileQ));
@@ -274,6 +322,15 @@ int launch_np(const Params& p, JoinMode mode, const JoinArgs& a, bool sym, cudaS
 }
 
 }  // namespace
+
+int count_tests(const Index* ix, const JoinArgs& a, unsigned long long* d_out, cudaStream_t s) {
+    if (a.n_tiles <= 0) return GJ_OK;
+    const Params p = join_params(ix);
+    k_count_tests<<<grid_ctas(a, (int)p.tile_q, kTileQ), kTileQ, 0, s>>>(p, a, ix->opt.symmetric, d_out);
+    count_launch();
+    GJ_CUDA(cudaGetLastError());
+    return GJ_OK;
+}
 
 JoinParams join_params(const Index* ix) {
     JoinParams p;

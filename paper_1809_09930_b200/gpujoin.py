@@ -20,7 +20,7 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 # Every symbol include/gpujoin.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
            "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_tc_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
-           "gj_self_join_host", "gj_join_stats", "gj_neighbor_table", "gj_free_index", "gj_last_error",
+           "gj_self_join_host", "gj_join_stats", "gj_join_counts", "gj_neighbor_table", "gj_free_index", "gj_last_error",
            "gj_abi_version", "gj_launch_count", "gj_release_cached_memory"]
 
 
@@ -78,6 +78,7 @@ def lib():
         "gj_self_join": (C.c_int, [P, P, I64, I32, I32, C.POINTER(I64)]),
         "gj_self_join_host": (C.c_int, [P, P, I64, I32, I32, I64, C.POINTER(I64), C.POINTER(C.c_int32)]),
         "gj_join_stats": (C.c_int, [P, I32, I32, C.POINTER(Stats)]),
+        "gj_join_counts": (C.c_int, [P, I32, I32, C.POINTER(Stats)]),
         "gj_neighbor_table": (C.c_int, [P, P, I64, P]),
         "gj_free_index": (None, [P]),
         "gj_last_error": (C.c_char_p, []),
@@ -214,6 +215,12 @@ class Index:
         _check(lib().gj_join_stats(self._h, rank, world, C.byref(s)))
         return dict(cells=s.cells, tests=s.tests, dims=s.dims, pairs=s.pairs, tests_evaluated=s.tests_evaluated,
                     dims_evaluated=s.dims_evaluated)
+
+    def counts(self, rank=0, world=1) -> dict:
+        """cells / tests / tests_evaluated without the distance work (gj_join_counts)."""
+        s = Stats()
+        _check(lib().gj_join_counts(self._h, rank, world, C.byref(s)))
+        return dict(cells=s.cells, tests=s.tests, tests_evaluated=s.tests_evaluated)
 
     def neighbor_table(self, pairs, n_pairs, offsets):
         _check(lib().gj_neighbor_table(self._h, _ptr(pairs), int(n_pairs), _ptr(offsets)))

@@ -208,12 +208,28 @@ def test_work_counters_equal_oracle(gen, count, dims, eps, k, symmetric):
     assert st["cells"] == cnt["cells"]
     assert st["tests"] == cnt["tests"]
     assert st["dims"] == cnt["dims"]
+    c = ix.counts()   # gj_join_counts: the same counters without the distance work
+    assert (c["cells"], c["tests"], c["tests_evaluated"]) == (st["cells"], st["tests"], st["tests_evaluated"])
     assert st["pairs"] == len(P)
     if symmetric:   # each unordered pair once; the self test is not evaluated
         assert 2 * st["tests_evaluated"] + count == cnt["tests"]
         assert 2 * st["dims_evaluated"] + count * dims == cnt["dims"]
     else:
         assert st["tests_evaluated"] == cnt["tests"] and st["dims_evaluated"] == cnt["dims"]
+
+
+@pytest.mark.parametrize("sortidu", [0, 1])
+@pytest.mark.parametrize("symmetric", [0, 1])
+@pytest.mark.parametrize("mma_tiles", [1, 2])
+def test_join_counts_equal_stats_scan(sortidu, symmetric, mma_tiles):
+    """gj_join_counts (binary-searched SORTIDU windows) == the FP64 stats scan's
+    cells / tests / tests_evaluated, for 128- and 256-query tiles, per rank."""
+    D = synth.exponential(5000, 24, seed=11)
+    from paper_1809_09930_b200 import Index
+    ix = Index(torch.from_numpy(D).cuda(), 0.07, 4, sortidu=sortidu, symmetric=symmetric, mma_tiles=mma_tiles)
+    for rank, world in [(0, 1), (0, 2), (1, 2)]:
+        st, c = ix.stats(rank, world), ix.counts(rank, world)
+        assert (c["cells"], c["tests"], c["tests_evaluated"]) == (st["cells"], st["tests"], st["tests_evaluated"])
 
 
 @pytest.mark.parametrize("symmetric", [0, 1])
@@ -252,6 +268,38 @@ def test_batches_and_host_pipeline_equal_single_launch():
     from paper_1809_09930_b200 import GpuJoinError
     with pytest.raises(GpuJoinError):
         ix.self_join(out[:10])
+
+
+_REGROW_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import synth
+from paper_1809_09930_b200 import Index
+D = synth.exponential(6000, 16, seed=9)
+ix = Index(torch.from_numpy(D).cuda(), 0.045, 6)
+cap = ix.estimate(1.0) + 4096
+out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+n = ix.self_join(out)
+ref = sorted(map(tuple, out[:n].cpu().numpy().tolist()))
+for pinned in (False, True):
+    host = torch.empty((cap, 2), dtype=torch.int32, pin_memory=pinned)
+    m, nb = ix.self_join_host(host, batch_size=max(1, n // 5))
+    assert m == n and nb >= 5, (m, n, nb)
+    assert sorted(map(tuple, host[:m].numpy().tolist())) == ref
+print("regrow ok", n, nb)
+"""
+
+
+def test_host_pipeline_regrows_underestimated_batches():
+    """GJ_BATCH_HEADROOM=0.05 makes every result slot far too small for its
+    batch: each slot is regrown on its own and the batch rerun (§3.2.2), the
+    pairs identical to one device launch."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GJ_BATCH_HEADROOM="0.05")
+    r = subprocess.run([sys.executable, "-c", _REGROW_SCRIPT, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "regrow ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_neighbor_table():
