@@ -64,7 +64,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stats", action="store_true",
                    help="skip the FP64 work-counter pass (roofline = null); for large sweep workloads")
-    p.add_argument("--cpu-sample", type=int, default=24, help="oracle query sample for cpu_baseline")
+    p.add_argument("--cpu-sample", type=int, default=96,
+                   help="oracle query sample for cpu_baseline (~13 s on expo32; the reference arm uses a quarter per step)")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu baseline/clocks")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo lets several ranks share one GPU "
                    "to exercise the multi-rank path on a 1-GPU box")
