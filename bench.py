@@ -59,7 +59,8 @@ def parse():
                    help="0 FP64 scan, 1 FP32 certified prefilter, 2 tcgen05 certified bound, 3 mma.sync bound")
     p.add_argument("--mma-tiles", type=int, default=0, choices=[0, 1, 2],
                    help="filter 2: 128-query accumulator tiles per tcgen05 CTA (0 = library default, 1)")
-    p.add_argument("--batch-size", type=int, default=100_000_000)
+    p.add_argument("--batch-size", type=int, default=0,
+                   help="result batch size b_s in pairs (0 = sized against free HBM, R15; the paper used 1e8)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stats", action="store_true",

@@ -272,8 +272,20 @@ int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t stream) {
     return selftest_umma(A, B, D, (cudaStream_t)stream);
 }
 
+// b_s sized against device memory (reading R15): the paper's 1e8 pairs was
+// sized for 2018 GPUs; a B200 holds ~2e10 pairs.
+static int64_t auto_batch_size() {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return 100000000ll;
+    }
+    const int64_t bs = (int64_t)(free_b / 4 / 3 / 8);
+    return std::max<int64_t>(100000000ll, bs);
+}
+
 int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size) {
-    if (batch_size <= 0) batch_size = 100000000ll;
+    if (batch_size <= 0) batch_size = auto_batch_size();
     int64_t nb = (std::max<int64_t>(est_pairs, 0) + batch_size - 1) / batch_size;
     return std::max<int64_t>(3, nb);
 }
@@ -354,7 +366,7 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
     if (!h || !n_pairs || (capacity > 0 && !out_pairs) || capacity < 0) { set_error("bad argument"); return GJ_ERR_INVALID; }
     if (int rc = check_rank(rank, world)) return rc;
     Index& ix = h->ix;
-    if (batch_size <= 0) batch_size = 100000000ll;
+    if (batch_size <= 0) batch_size = auto_batch_size();
     int64_t est = 0;
     if (int rc = gj_estimate(h, 0.01, rank, world, &est)) return rc;
     const int64_t nb = gj_num_batches(est, batch_size);

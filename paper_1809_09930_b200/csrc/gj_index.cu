@@ -609,6 +609,13 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaGetLastError());
     if ((rc = varying_bits_u64(skey, T, &vb, s))) return rc;
     if ((rc = radix_sort_u64(skey, ix->tile_order, T, vb, s))) return rc;
+    // host copy of the heaviest-first work (keys are ~work) for work-balanced split plans
+    ix->h_work_by_pos.resize((size_t)T);
+    if (T > 0) {
+        GJ_CUDA(cudaMemcpyAsync(ix->h_work_by_pos.data(), skey, (size_t)T * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        GJ_CUDA(cudaStreamSynchronize(s));
+        for (auto& w : ix->h_work_by_pos) w = ~w;
+    }
     unsigned long long h_total = 0;
     GJ_CUDA(cudaMemcpyAsync(&h_total, d_total, sizeof(h_total), cudaMemcpyDeviceToHost, s));
     GJ_CUDA(pool_malloc(&ix->scratch_count, 8 * sizeof(uint64_t), s));

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/gpujoin.h"
 
@@ -84,6 +85,7 @@ struct Index {
     uint32_t* tile_q0 = nullptr;     // [T]
     uint32_t* tile_order = nullptr;  // [T] tiles, heaviest estimated work first
     uint64_t* tile_work = nullptr;   // [T] queries * candidates (pre-SORTIDU)
+    std::vector<uint64_t> h_work_by_pos;   // host: tile_work of tile_order[j] (work-balanced split plans)
     Meta* meta = nullptr;            // device
     uint64_t* scratch_count = nullptr;   // [4] device counters
     Meta h_meta{};                   // host copy
@@ -121,6 +123,10 @@ struct JoinArgs {
     int64_t step;             // tile positions j = first + step * m
     int64_t n_tiles;          // number of m values
     int32_t split;            // CTAs per tile, each scanning 1/split of every candidate window (0/1 = none)
+    // Work-balanced split (optional, overrides split): tile m of the launch gets
+    // part_off[m+1] - part_off[m] CTAs; part_off[n_tiles] = total parts.
+    const uint32_t* part_off;
+    int64_t total_parts;
 };
 struct JoinParams {
     const double* __restrict__ pts;
@@ -151,16 +157,32 @@ struct JoinParams {
 // nq = 0 marks an empty sub-block (the tile's cell ended earlier).
 struct CtaTile {
     uint32_t g, q0, nq;
-    int part;
+    int part, split;
 };
 __device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs& A, uint32_t qper) {
-    const uint32_t split = A.split > 1 ? (uint32_t)A.split : 1u;
     const uint32_t subs = P.tile_q > qper ? P.tile_q / qper : 1u;
     CtaTile t;
-    t.part = (int)(blockIdx.x % split);
-    const uint32_t m = blockIdx.x / split;
-    const uint32_t sub = m % subs;
-    const int64_t j = A.first + A.step * (int64_t)(m / subs);
+    uint32_t m, sub;
+    if (A.part_off) {   // CTA b: (unit r = b / subs, sub = b % subs), unit r -> (tile m, part)
+        sub = blockIdx.x % subs;
+        const uint32_t r = blockIdx.x / subs;
+        uint32_t lo = 0, hi = (uint32_t)A.n_tiles;   // last m with part_off[m] <= r
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (A.part_off[mid] <= r) lo = mid; else hi = mid;
+        }
+        m = lo;
+        t.part = (int)(r - A.part_off[m]);
+        t.split = (int)(A.part_off[m + 1] - A.part_off[m]);
+    } else {
+        const uint32_t split = A.split > 1 ? (uint32_t)A.split : 1u;
+        t.part = (int)(blockIdx.x % split);
+        t.split = (int)split;
+        const uint32_t mm = blockIdx.x / split;
+        sub = mm % subs;
+        m = mm / subs;
+    }
+    const int64_t j = A.first + A.step * (int64_t)m;
     const uint32_t tile = P.tile_order[j];
     t.g = P.tile_cell[tile];
     t.q0 = P.tile_q0[tile] + sub * qper;
@@ -171,6 +193,7 @@ __device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs&
 // CTAs of a launch over a.n_tiles index tiles with `qper` queries per CTA.
 inline unsigned grid_ctas(const JoinArgs& a, int tile_q, int qper) {
     const int64_t subs = tile_q > qper ? tile_q / qper : 1;
+    if (a.part_off) return (unsigned)(a.total_parts * subs);
     return (unsigned)(a.n_tiles * subs * (a.split > 1 ? a.split : 1));
 }
 JoinParams join_params(const Index* ix);

@@ -25,6 +25,10 @@
 // data-dependent early exit, not a dense contraction (north_star).
 #include <stdlib.h>
 
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "gj_internal.cuh"
 
 namespace gj {
@@ -65,10 +69,9 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
     // split-K over candidates: CTA (m, part) scans part `part` of every window
-    const int split = A.split > 1 ? A.split : 1;
     const CtaTile ct = cta_tile(P, A, kTileQ);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
-    const int part = ct.part;
+    const int part = ct.part, split = ct.split;
     const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
     const bool active = tid < (int)nq;
     const uint32_t qpos = q0 + (active ? tid : 0);
@@ -369,7 +372,51 @@ void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank
     a->n_tiles = a->first < ix->T ? (ix->T - a->first + a->step - 1) / a->step : 0;
 }
 
-int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
+// Work-balanced split plan of one launch: a tile whose estimated work
+// (queries x candidates) exceeds W / (148 x 8) of the launch's total W is
+// scanned by ceil(work / that) CTAs (each 1/parts of every candidate window),
+// so a batch never waits on one heavy tile (clustered data: a few dense cells
+// carry most of the work, and round-robin batching puts one in every batch).
+// Returns false when every tile gets one CTA.
+static bool plan_parts(const Index* ix, const JoinArgs& a, std::vector<uint32_t>* off) {
+    if (a.n_tiles <= 0 || a.split > 1 || ix->h_work_by_pos.size() != (size_t)ix->T) return false;
+    double W = 0.0, wmax = 0.0;
+    for (int64_t m = 0; m < a.n_tiles; ++m) {
+        const double w = (double)ix->h_work_by_pos[(size_t)(a.first + a.step * m)];
+        W += w;
+        wmax = w > wmax ? w : wmax;
+    }
+    const double target = W / (148.0 * 8.0);
+    if (!(target > 0.0) || wmax <= target) return false;
+    off->resize((size_t)a.n_tiles + 1);
+    uint64_t acc = 0;
+    for (int64_t m = 0; m < a.n_tiles; ++m) {
+        (*off)[(size_t)m] = (uint32_t)acc;
+        const double w = (double)ix->h_work_by_pos[(size_t)(a.first + a.step * m)];
+        acc += (uint64_t)std::min(512.0, std::max(1.0, std::ceil(w / target)));
+    }
+    (*off)[(size_t)a.n_tiles] = (uint32_t)acc;
+    return true;
+}
+
+static int launch_join_planned(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+
+int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a0, cudaStream_t s) {
+    std::vector<uint32_t> off;
+    if (mode == kStats || a0.part_off || !plan_parts(ix, a0, &off)) return launch_join_planned(ix, mode, a0, s);
+    JoinArgs a = a0;
+    uint32_t* d_off = nullptr;
+    GJ_CUDA(pool_malloc(&d_off, off.size() * sizeof(uint32_t), s));
+    // pageable source: the copy is staged before the call returns
+    GJ_CUDA(cudaMemcpyAsync(d_off, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    a.part_off = d_off;
+    a.total_parts = (int64_t)off.back();
+    const int rc = launch_join_planned(ix, mode, a, s);
+    GJ_CUDA(cudaFreeAsync(d_off, s));
+    return rc;
+}
+
+static int launch_join_planned(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     if (ix->filter == 2 && mode != kStats) return launch_join_umma(ix, mode, a, s);
     if (ix->filter == 3 && mode != kStats) return launch_join_tc(ix, mode, a, s);
     if (ix->filter == 1 && mode != kStats) return launch_join32(ix, mode, a, s);

@@ -50,10 +50,9 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
     // split-K over candidates: CTA (m, part) scans part `part` of every window
-    const int split = A.split > 1 ? A.split : 1;
     const CtaTile ct = cta_tile(P, A, kTileQ);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
-    const int part = ct.part;
+    const int part = ct.part, split = ct.split;
     const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
     const bool active = tid < (int)nq;
     const uint32_t qpos = q0 + (active ? tid : 0);

@@ -104,10 +104,9 @@ __global__ void __launch_bounds__(kTileQ) k_join_tc(JoinParams P, JoinArgs A) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gq = lane >> 2, tq = lane & 3;
-    const int split = A.split > 1 ? A.split : 1;
     const CtaTile ct = cta_tile(P, A, kTileQ);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
-    const int part = ct.part;
+    const int part = ct.part, split = ct.split;
     const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
     const int n_pad = P.n_pad;
     const double eps = P.eps;

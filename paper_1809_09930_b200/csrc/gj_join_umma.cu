@@ -143,8 +143,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
     const CtaTile ct = cta_tile(P, A, QT);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int split = A.split > 1 ? A.split : 1;
-    const int part = ct.part;
+    const int part = ct.part, split = ct.split;
     const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
     const int nsub = (int)((nq + kM - 1) / kM);   // A tiles holding queries (1..MT)
     const int n_pad = P.n_pad;

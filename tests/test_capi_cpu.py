@@ -51,7 +51,7 @@ def test_host_only_entry_points(L):
     assert pkg.num_batches(3 * 10 ** 8, 10 ** 8) == 3
     assert pkg.num_batches(10 ** 5, 10 ** 8) == 3
     assert pkg.num_batches(10 ** 9, 10 ** 8) == 10
-    assert pkg.num_batches(10 ** 9, 0) == 10          # default b_s = 1e8
+    assert pkg.num_batches(10 ** 9, 0) == 10          # auto b_s: no device here -> the paper's 1e8
 
 
 def test_invalid_arguments_fail_without_touching_the_gpu(L):

@@ -23,7 +23,7 @@ def _lib():
     __graft_entry__.build()
 
 
-def bench_launch(ix, rank=0, world=1, b_s=100_000_000):
+def bench_launch(ix, rank=0, world=1, b_s=0):
     """Exactly bench.py's step after the index build."""
     from paper_1809_09930_b200 import num_batches
     est = ix.estimate(0.01, rank, world)
