@@ -146,6 +146,12 @@ GJ_API int gj_estimate(gj_index* idx, double frac, int32_t rank, int32_t world, 
  * Returns 1 if the filter is enabled for such data, 0 if not, <0 on error. */
 GJ_API int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, double* margin);
 
+/* Certain-inside side of the same FP32 analysis (host only): a float32 running sum
+ * <= *thr_in proves dist(a, b) <= eps (1 - 1e-9), so filter 1 accepts such a pair
+ * without the FP64 test (the FP64 test would accept it too).  *thr_in = -1 when the
+ * spread leaves no such region.  GJ_OK or GJ_ERR_INVALID. */
+GJ_API int gj_fp32_accept_threshold(double eps, int32_t n, const double* spans, float* thr_in);
+
 /* Host only: threshold T of the certified tensor-core bound (filter 2/3) for
  * radius eps, n coordinates, MMA depth K (>= n + 4), power-of-two scale S and
  * R2 = max squared norm of the fp16 operand rows.  The kernel rejects a pair

@@ -259,6 +259,12 @@ int gj_fp32_threshold(double eps, int32_t n, const double* spans, float* thr, do
     return fp32_threshold_from_spans(eps, n, spans, thr, margin);
 }
 
+int gj_fp32_accept_threshold(double eps, int32_t n, const double* spans, float* thr_in) {
+    if (!spans || !thr_in || n < 1 || n > kMaxDim || !(eps > 0.0)) { set_error("bad argument"); return GJ_ERR_INVALID; }
+    *thr_in = fp32_accept_threshold_from_spans(eps, n, spans);
+    return GJ_OK;
+}
+
 int gj_tc_threshold(double eps, int32_t n, int32_t K, double S, double R2, double* thr, double* margin) {
     if (!thr || !margin || n < 1 || K < n + 4 || !(eps > 0.0) || !(S > 0.0) || !(R2 >= 0.0)) {
         set_error("bad argument");

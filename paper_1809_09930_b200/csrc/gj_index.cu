@@ -361,10 +361,29 @@ int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr
     return (smax < 1e30) && (T32 < 1e30f) && !(A > 1e-3 * eps);
 }
 
+float fp32_accept_threshold_from_spans(double eps, int n, const double* spans) {
+    // Certain-inside side of the same analysis: the float32 running sum is
+    // >= (1 - gamma_n) ||t||^2 and ||q - c|| <= ||t|| + A, so a final sum
+    // <= (1 - gamma_n)(eps (1 - 1e-9) - A)^2 proves dist <= eps (1 - 1e-9): the
+    // FP64 test would accept it too.  Rounded down; -1 (never) if A >= eps.
+    double ss = 0.0;
+    for (int t = 0; t < n; ++t) ss += spans[t] * spans[t];
+    const double u = std::ldexp(1.0, -24);
+    const double A = 4.001 * u * std::sqrt(ss) * (1.0 + 1e-12) + std::sqrt((double)n) * std::ldexp(1.0, -147);
+    const double gamma = n * u / (1.0 - n * u);
+    const double r = eps * (1.0 - 1e-9) - A;
+    if (!(r > 0.0) || !std::isfinite(r)) return -1.0f;
+    const double T = (1.0 - gamma) * r * r;
+    float T32 = (float)T;
+    if ((double)T32 > T) T32 = std::nextafter(T32, -INFINITY);
+    return T32;
+}
+
 static bool fp32_threshold(Index* ix) {
     const Meta& m = ix->h_meta;
     double spans[kMaxDim];
     for (int t = 0; t < ix->n; ++t) spans[t] = m.maxs[m.order[t]] - m.mins[m.order[t]];
+    ix->thr32_in = fp32_accept_threshold_from_spans(ix->eps, ix->n, spans);
     return fp32_threshold_from_spans(ix->eps, ix->n, spans, &ix->thr32, &ix->filter_margin) != 0;
 }
 

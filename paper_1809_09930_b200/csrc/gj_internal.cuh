@@ -67,6 +67,7 @@ struct Index {
     float* pts32 = nullptr;          // [N][n_pad] fl32(x - min_j): input of the certified FP32 prefilter
     int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tcgen05 bound, 3 mma.sync bound (+ FP64 decision)
     float thr32 = 0.f;               // FP32 prefilter rejection threshold (> eps^2, see fp32_threshold)
+    float thr32_in = -1.f;           // FP32 certain-inside threshold (< eps^2): accepted without the FP64 test
     double filter_margin = 0;        // thr32 / eps^2 - 1
     __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)) + candidate-side augmented columns
     double* norm16 = nullptr;        // [N] ||fp16 coordinates||^2 (exact, fp64)
@@ -109,6 +110,7 @@ int varying_bits_u64(const uint64_t* keys, int64_t n, uint64_t* h_out, cudaStrea
 // Certified FP32 prefilter threshold from the per-dim spans (max - min);
 // returns 0 when the filter cannot be certified usefully.
 int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr, double* margin);
+float fp32_accept_threshold_from_spans(double eps, int n, const double* spans);
 // Certified tensor-core bound threshold (scaled units); returns 0 if not useful.
 int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr, double* margin);
 int build_index(Index* ix, const double* d_points);
@@ -141,7 +143,7 @@ struct JoinParams {
     const uint32_t* __restrict__ tile_order;
     int n, n_pad, u, sortidu, shortc;
     double eps, eps2;
-    float thr32;
+    float thr32, thr32_in;
     const __half* __restrict__ pts16;
     const double* __restrict__ norm16;
     int k16;

@@ -355,6 +355,7 @@ JoinParams join_params(const Index* ix) {
     p.eps = ix->eps;
     p.eps2 = ix->eps2;
     p.thr32 = ix->thr32;
+    p.thr32_in = ix->thr32_in;
     p.pts16 = ix->pts16;
     p.norm16 = ix->norm16;
     p.k16 = ix->k16;

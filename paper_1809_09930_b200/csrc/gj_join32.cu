@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
         q[d + 3] = make_float2(v.w, v.w);
     }
     const double eps = P.eps, eps2 = P.eps2;
-    const float thr = P.thr32;
+    const float thr = P.thr32, thr_in = P.thr32_in;
     const uint32_t qid = P.orig[qpos];
     const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
@@ -169,9 +169,11 @@ __global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
                 }
                 const float a0 = a.x, a1 = a.y;
                 // survivors of the prefilter: decided in FP64
+                // ... unless the bound also proves them inside (a <= thr_in): on dense
+                // data almost every candidate is a pair and skips the FP64 row reads
                 bool hit0 = ok0 && a0 <= thr, hit1 = ok1 && a1 <= thr;
-                if (hit0) hit0 = dist2_fp64(qrow64, P.pts + (size_t)p0 * n_pad, n_pad) <= eps2;
-                if (hit1) hit1 = dist2_fp64(qrow64, P.pts + (size_t)(p0 + 1) * n_pad, n_pad) <= eps2;
+                if (hit0 && !(a0 <= thr_in)) hit0 = dist2_fp64(qrow64, P.pts + (size_t)p0 * n_pad, n_pad) <= eps2;
+                if (hit1 && !(a1 <= thr_in)) hit1 = dist2_fp64(qrow64, P.pts + (size_t)(p0 + 1) * n_pad, n_pad) <= eps2;
                 if (MODE == kEmit) {
                     const unsigned m0 = __ballot_sync(0xffffffffu, hit0);
                     const unsigned m1 = __ballot_sync(0xffffffffu, hit1);

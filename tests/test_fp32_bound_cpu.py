@@ -68,6 +68,37 @@ def test_no_inside_pair_is_rejected(n, eps, span, shift):
             assert s <= thr
 
 
+@pytest.mark.parametrize("n,eps,span,shift", [(8, 0.05, 1.0, 0.0), (32, 0.08, 1.0, 0.0), (90, 0.01, 1.0, 0.0),
+                                              (24, 1e-2, 1.0, 1000.0)])
+def test_no_outside_pair_is_accepted_without_fp64(n, eps, span, shift):
+    """gj_fp32_accept_threshold: a pair whose exact distance is at or beyond
+    eps (1 - 1e-9) never has a float32 sum <= thr_in (it must go to the FP64
+    test); pairs well inside are accepted (the threshold is useful)."""
+    rng = np.random.default_rng(n + 7)
+    mins = np.full(n, shift)
+    thr_in = gpujoin.fp32_accept_threshold(eps, np.full(n, span))
+    enabled, thr, _ = gpujoin.fp32_threshold(eps, np.full(n, span))
+    if not enabled:
+        pytest.skip("filter disabled for this spread")
+    assert 0 < float(thr_in) < eps * eps < float(thr)
+    T = Fraction(float(thr_in))
+    lim = Fraction(eps) * (1 - Fraction(1, 10 ** 9))
+    n_inside_ok = 0
+    for i in range(240):
+        q = shift + rng.random(n) * span
+        v = rng.standard_normal(n)
+        v /= np.linalg.norm(v)
+        rel = [1 - 5e-10, 1.0, 1 + 1e-7, 0.999][i % 4]       # at / beyond the certain-inside limit, and well inside
+        c = np.clip(q + v * eps * rel, shift, shift + span)
+        d2 = sum((Fraction(float(a)) - Fraction(float(b))) ** 2 for a, b in zip(q, c))
+        final = kernel_sums(q, c, mins)[-1]
+        if d2 >= lim * lim:
+            assert final > T, "an outside / boundary pair would skip the FP64 test"
+        elif d2 <= (Fraction(eps) * Fraction(999, 1000)) ** 2 * Fraction(1001, 1000):
+            n_inside_ok += final <= T
+    assert n_inside_ok > 30
+
+
 def test_threshold_margin_and_switch_off():
     on, thr, margin = gpujoin.fp32_threshold(0.08, np.full(32, 0.4))
     assert on and 0 < margin < 1e-4 and float(thr) >= 0.08 ** 2
