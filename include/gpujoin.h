@@ -159,12 +159,6 @@ GJ_API int gj_fp32_accept_threshold(double eps, int32_t n, const double* spans, 
  * implies dist > eps (1 + 1e-9).  Returns 1 if usable, 0 if not, <0 on error. */
 GJ_API int gj_tc_threshold(double eps, int32_t n, int32_t K, double S, double R2, double* thr, double* margin);
 
-/* Certain-inside side of the tensor-core bound (host only): an accumulator
- * >= *acc_in proves dist <= eps (1 - 1e-9), so filter 2 accepts the pair without
- * the FP64 test.  T = gj_tc_threshold's threshold.  *acc_in = +inf when there is
- * no such region.  GJ_OK or GJ_ERR_INVALID. */
-GJ_API int gj_tc_accept_threshold(double eps, int32_t n, int32_t K, double S, double R2, double T, float* acc_in);
-
 /* Diagnostic: D[128][128] = A[128][32] . B[128][32]^T (fp16 row-major device
  * inputs, fp32 row-major device output) through the join kernel's tcgen05 /
  * TMEM path (shared-memory layout, descriptors, TMEM load).  Synchronous. */

@@ -265,12 +265,6 @@ int gj_fp32_accept_threshold(double eps, int32_t n, const double* spans, float* 
     return GJ_OK;
 }
 
-int gj_tc_accept_threshold(double eps, int32_t n, int32_t K, double S, double R2, double T, float* acc_in) {
-    if (!acc_in || n < 1 || K < n + 4 || !(eps > 0.0) || !(S > 0.0) || !(R2 >= 0.0)) { set_error("bad argument"); return GJ_ERR_INVALID; }
-    *acc_in = tc_accept_from(eps, n, K, S, R2, T);
-    return GJ_OK;
-}
-
 int gj_tc_threshold(double eps, int32_t n, int32_t K, double S, double R2, double* thr, double* margin) {
     if (!thr || !margin || n < 1 || K < n + 4 || !(eps > 0.0) || !(S > 0.0) || !(R2 >= 0.0)) {
         set_error("bad argument");

@@ -420,26 +420,6 @@ int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr
     return std::isfinite(T) && *margin < 0.25 && T < 40000.0 && R2 < 40000.0;
 }
 
-// Certain-inside side of the same bound: with |acc - (T - ||q^ - c^||^2)/2| <= a + b T,
-// acc >= A_in = (T + 2a + 2bT - r_in^2)/2, r_in = S eps (1 - 1e-9) - delta, gives
-// ||q^ - c^|| <= r_in and so dist <= eps (1 - 1e-9): the FP64 test would accept the
-// pair too.  Returned as a float rounded up; +inf when no such region exists.
-float tc_accept_from(double eps, int n, int K, double S, double R2, double T) {
-    const double u11 = std::ldexp(1.0, -11);
-    const double R = std::sqrt(R2);
-    const double Rp = (R + std::sqrt((double)n) * std::ldexp(1.0, -25)) / (1.0 - u11);
-    const double delta = u11 * 2.0 * Rp + std::sqrt((double)n) * std::ldexp(1.0, -24);
-    const double kappa = (K + 2) * std::ldexp(1.0, -21);
-    const double a = kappa * 2.001 * R2 + std::ldexp(1.0, -22) * R2 + std::ldexp(1.0, -23) + std::ldexp(1.0, -51) * R2;
-    const double b = 0.5005 * kappa + std::ldexp(1.0, -23) + std::ldexp(1.0, -51);
-    const double r_in = S * eps * (1.0 - 1e-9) - delta;
-    if (!(r_in > 0.0) || !std::isfinite(T)) return INFINITY;
-    const double A = (T + 2.0 * a + 2.0 * b * T - r_in * r_in) * 0.5 * (1.0 + 1e-9) + 1e-30;
-    float A32 = (float)A;
-    if ((double)A32 < A) A32 = std::nextafter(A32, INFINITY);
-    return A32;
-}
-
 namespace {
 // pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond (one thread per element).
 __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, int k16, double S,
@@ -516,7 +496,6 @@ static int make_fp16(Index* ix, bool* ok) {
     double R2;
     memcpy(&R2, &h_r2, sizeof(R2));
     *ok = tc_threshold_from(ix->eps, ix->n, ix->k16, ix->tc_scale, R2, &ix->thr16, &ix->margin16) != 0;
-    ix->acc_in16 = tc_accept_from(ix->eps, ix->n, ix->k16, ix->tc_scale, R2, ix->thr16);
     if (!*ok) {
         GJ_CUDA(cudaFreeAsync(ix->pts16, s));
         GJ_CUDA(cudaFreeAsync(ix->norm16, s));

@@ -2,7 +2,6 @@
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
-#include <math.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -76,7 +75,6 @@ struct Index {
     int tile_q = kTileQ;             // queries per tile: 128, or 256 for the M = 2 x 128 tcgen05 kernel
     double tc_scale = 1.0;           // S, a power of two
     double thr16 = 0.0;              // tensor-core bound threshold T (scaled units)
-    float acc_in16 = INFINITY;       // accumulator >= this: certainly inside (no FP64 test)
     double margin16 = 0;             // thr16 / (S eps)^2 - 1
     uint32_t* orig = nullptr;        // [N] sorted position -> original id
     uint64_t* cell_id = nullptr;     // [G] sorted non-empty linear ids
@@ -115,7 +113,6 @@ int fp32_threshold_from_spans(double eps, int n, const double* spans, float* thr
 float fp32_accept_threshold_from_spans(double eps, int n, const double* spans);
 // Certified tensor-core bound threshold (scaled units); returns 0 if not useful.
 int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr, double* margin);
-float tc_accept_from(double eps, int n, int K, double S, double R2, double T);
 int build_index(Index* ix, const double* d_points);
 
 // ---- join (gj_join.cu) ----
@@ -151,7 +148,6 @@ struct JoinParams {
     const double* __restrict__ norm16;
     int k16;
     double thr16;
-    float acc_in;                    // tcgen05 epilogue: accumulator >= acc_in -> accepted without FP64 (+inf: off)
     uint32_t tile_q;                 // queries per index tile (128 or 256)
     int debug;                       // timing experiments only (GJ_DEBUG_UMMA); 0 in production
 };

@@ -360,8 +360,6 @@ JoinParams join_params(const Index* ix) {
     p.norm16 = ix->norm16;
     p.k16 = ix->k16;
     p.thr16 = ix->thr16;
-    // staged survivors carry the certain-inside flag in bit 31 of the query position
-    p.acc_in = ix->N < (int64_t)0x80000000ll ? ix->acc_in16 : INFINITY;
     p.tile_q = (uint32_t)ix->tile_q;
     static const int dbg = [] { const char* e = getenv("GJ_DEBUG_UMMA"); return e ? atoi(e) : 0; }();
     p.debug = dbg;

@@ -46,11 +46,8 @@ __device__ __forceinline__ unsigned long long decide_batch(const JoinParams& P, 
                                                            uint32_t n, int lane) {
     constexpr unsigned long long kMul = SYM ? 2ull : 1ull;
     const bool has = (uint32_t)lane < n;
-    uint2 e = has ? sv[lane] : make_uint2(0u, 0u);
-    const bool sure = (e.x >> 31) != 0;   // the bound proved it inside: no FP64 test
-    e.x &= 0x7fffffffu;
-    const bool ok = has && (sure || dist2_fp64(P.pts + (size_t)e.x * P.n_pad, P.pts + (size_t)e.y * P.n_pad,
-                                               P.n_pad) <= P.eps2);
+    const uint2 e = has ? sv[lane] : make_uint2(0u, 0u);
+    const bool ok = has && dist2_fp64(P.pts + (size_t)e.x * P.n_pad, P.pts + (size_t)e.y * P.n_pad, P.n_pad) <= P.eps2;
     if (MODE != kEmit) return ok ? kMul : 0ull;
     const unsigned m = __ballot_sync(0xffffffffu, ok);
     if (!m) return 0ull;
@@ -313,7 +310,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
                     // CW columns in chunks of <= 64 (two loads in flight, one wait); the
                     // accumulator is released right after the last wait.  Survivors:
                     // mask bit j of word h = column 64 h + j.
-                    unsigned long long mask[2] = {0, 0}, sure[2] = {0, 0};
+                    unsigned long long mask[2] = {0, 0};
 #pragma unroll
                     for (int h = 0; h < (NL + 1) / 2; ++h) {
                         constexpr int NC = NL < 2 ? NL : 2;
@@ -344,10 +341,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
                             for (int x = 0; x < NC; ++x)
 #pragma unroll
                                 for (int y = 0; y < 32; ++y)
-                                    if (!(v[x][y] >> 31)) {
-                                        mask[h] |= 1ull << (32 * x + y);
-                                        if (__uint_as_float(v[x][y]) >= P.acc_in) sure[h] |= 1ull << (32 * x + y);
-                                    }
+                                    if (!(v[x][y] >> 31)) mask[h] |= 1ull << (32 * x + y);
                         }
                     }
                     if (!__any_sync(0xffffffffu, (mask[0] | mask[1]) != 0ull)) continue;
@@ -356,17 +350,16 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
                     for (int hh = 0; hh < (NL + 1) / 2; ++hh) {
                         unsigned long long m = mask[hh];
                         while (__any_sync(0xffffffffu, m != 0ull)) {   // stage the survivors in [r, s)
-                            uint32_t cpos = 0, flag = 0;
+                            uint32_t cpos = 0;
                             bool has = false;
                             if (m) {
                                 const int bit = __ffsll((long long)m) - 1;
                                 m &= m - 1;
                                 cpos = base + 64 * hh + bit;
-                                flag = (uint32_t)((sure[hh] >> bit) & 1ull) << 31;
                                 has = !(cpos < wr || cpos >= wsd || (diag && cpos <= qpos));
                             }
                             const unsigned hb = __ballot_sync(0xffffffffu, has);
-                            if (has) sv[svn + __popc(hb & lt)] = make_uint2(qpos | flag, cpos);
+                            if (has) sv[svn + __popc(hb & lt)] = make_uint2(qpos, cpos);
                             svn += __popc(hb);
                             if (svn >= 32) {   // a full batch: one FP64 decision per lane
                                 __syncwarp();

@@ -19,7 +19,7 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 
 # Every symbol include/gpujoin.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
-           "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_fp32_accept_threshold", "gj_tc_threshold", "gj_tc_accept_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
+           "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_fp32_accept_threshold", "gj_tc_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
            "gj_self_join_host", "gj_join_stats", "gj_join_counts", "gj_neighbor_table", "gj_free_index", "gj_last_error",
            "gj_abi_version", "gj_launch_count", "gj_release_cached_memory"]
 
@@ -71,7 +71,6 @@ def lib():
         "gj_num_batches": (I64, [I64, I64]),
         "gj_selftest_umma": (C.c_int, [P, P, P, U64]),
         "gj_tc_threshold": (C.c_int, [D, I32, I32, D, D, C.POINTER(D), C.POINTER(D)]),
-        "gj_tc_accept_threshold": (C.c_int, [D, I32, I32, D, D, D, C.POINTER(C.c_float)]),
         "gj_fp32_threshold": (C.c_int, [D, I32, C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(D)]),
         "gj_fp32_accept_threshold": (C.c_int, [D, I32, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
         "gj_partition": (C.c_int, [I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
@@ -259,13 +258,6 @@ def fp32_threshold(eps: float, spans):
     if rc < 0:
         _check(rc)
     return bool(rc), np.float32(t.value), m.value
-
-
-def tc_accept_threshold(eps: float, n: int, K: int, S: float, R2: float, T: float):
-    """Certain-inside accumulator threshold of the tensor-core bound (+inf: none)."""
-    t = C.c_float()
-    _check(lib().gj_tc_accept_threshold(float(eps), int(n), int(K), float(S), float(R2), float(T), C.byref(t)))
-    return np.float32(t.value)
 
 
 def fp32_accept_threshold(eps: float, spans):
