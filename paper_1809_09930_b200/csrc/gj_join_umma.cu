@@ -138,7 +138,11 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
     constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, BN);
     constexpr uint32_t kSBO = KP * 16;
     constexpr uint32_t kBlockBytes = BN * KP * 2;
-    static_assert(NL >= 1 && NL <= 4, "epilogue columns per warp");
+    static_assert(NL >= 1 && NL <= 8, "epilogue columns per warp");
+    // TMEM loads in flight per wait: 4 (128 columns) when one warp reads a whole
+    // 256-column row (EPW = 1, 170 registers at two CTAs per SM), else 2
+    constexpr int NC = NL >= 8 ? 4 : (NL < 2 ? NL : 2);
+    constexpr int NMW = (NL + 1) / 2;       // 64-bit survivor mask words
 
     const CtaTile ct = cta_tile(P, A, QT);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
@@ -307,33 +311,34 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
                         if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
                         continue;
                     }
-                    // CW columns in chunks of <= 64 (two loads in flight, one wait); the
+                    // CW columns in chunks of NC x 32 (NC loads in flight, one wait); the
                     // accumulator is released right after the last wait.  Survivors:
-                    // mask bit j of word h = column 64 h + j.
-                    unsigned long long mask[2] = {0, 0};
+                    // mask bit j of word w = column 64 w + j.
+                    unsigned long long mask[NMW];
 #pragma unroll
-                    for (int h = 0; h < (NL + 1) / 2; ++h) {
-                        constexpr int NC = NL < 2 ? NL : 2;
+                    for (int w = 0; w < NMW; ++w) mask[w] = 0ull;
+#pragma unroll
+                    for (int h = 0; h < NL / NC; ++h) {
                         uint32_t v[NC][32];
 #pragma unroll
-                        for (int x = 0; x < NC; ++x) umma::tmem_ld32_nowait(tcol + 64 * h + 32 * x, v[x]);
+                        for (int x = 0; x < NC; ++x) umma::tmem_ld32_nowait(tcol + 32 * (NC * h + x), v[x]);
                         umma::tmem_wait_ld();
-                        if (h == (NL + 1) / 2 - 1) {
+                        if (h == NL / NC - 1) {
                             umma::fence_before();
                             __syncwarp();
                             if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
                         }
                         if (P.debug & 4) continue;   // timing experiment: reads only
                         // sign bits: balanced AND tree (short dependency chains)
-                        uint32_t t[16];
+                        uint32_t t[8 * NC];
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            const int e0 = (4 * k) % (32 * NC);
+                        for (int k = 0; k < 8 * NC; ++k) {
+                            const int e0 = 4 * k;
                             t[k] = v[e0 / 32][e0 % 32] & v[(e0 + 1) / 32][(e0 + 1) % 32] &
                                    v[(e0 + 2) / 32][(e0 + 2) % 32] & v[(e0 + 3) / 32][(e0 + 3) % 32];
                         }
 #pragma unroll
-                        for (int w = 8; w >= 1; w >>= 1)
+                        for (int w = 4 * NC; w >= 1; w >>= 1)
 #pragma unroll
                             for (int k = 0; k < w; ++k) t[k] &= t[k + w];
                         if (rvalid && !(t[0] >> 31)) {   // rare: some accumulator > +0
@@ -341,13 +346,17 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
                             for (int x = 0; x < NC; ++x)
 #pragma unroll
                                 for (int y = 0; y < 32; ++y)
-                                    if (!(v[x][y] >> 31)) mask[h] |= 1ull << (32 * x + y);
+                                    if (!(v[x][y] >> 31))
+                                        mask[(NC * h + x) >> 1] |= 1ull << (32 * ((NC * h + x) & 1) + y);
                         }
                     }
-                    if (!__any_sync(0xffffffffu, (mask[0] | mask[1]) != 0ull)) continue;
+                    unsigned long long anym = 0ull;
+#pragma unroll
+                    for (int w = 0; w < NMW; ++w) anym |= mask[w];
+                    if (!__any_sync(0xffffffffu, anym != 0ull)) continue;
                     const uint32_t base = rb + bi * BN + ecol * CW;
 #pragma unroll
-                    for (int hh = 0; hh < (NL + 1) / 2; ++hh) {
+                    for (int hh = 0; hh < NMW; ++hh) {
                         unsigned long long m = mask[hh];
                         while (__any_sync(0xffffffffu, m != 0ull)) {   // stage the survivors in [r, s)
                             uint32_t cpos = 0;
@@ -506,6 +515,7 @@ int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStre
     static const int cfg = [] { const char* e = getenv("GJ_UMMA_CFG"); return e ? atoi(e) : 0; }();
     if (ix->tile_q / kM == 2) return launch_umma_kp<128, 2, 2, 1>(ix, p, mode, a, sym, s);
     if (cfg == 2) return launch_umma_kp<128, 1, 2, 2>(ix, p, mode, a, sym, s);
+    if (cfg == 4) return launch_umma_kp<256, 1, 1, 1>(ix, p, mode, a, sym, s);
     if (cfg == 3) return launch_umma_kp<256, 1, 2, 4>(ix, p, mode, a, sym, s);
     return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
 }

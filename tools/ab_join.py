@@ -1,0 +1,28 @@
+"""A/B timing of two builds of the package (copies under abtest/<v>/, git-ignored):
+python tools/ab_join.py abtest/A [reps]"""
+import os, sys
+pkg = os.path.abspath(sys.argv[1])
+sys.path.insert(0, pkg)
+sys.path.insert(1, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+from paper_1809_09930_b200 import Index
+w = synth.WORKLOADS["expo32"]
+D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
+import paper_1809_09930_b200 as P
+assert P.__file__.startswith(pkg), P.__file__
+ts = []
+for r in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
+    ix = Index(D, w["eps"], w["k"])
+    est = ix.estimate(1.0)
+    out = torch.empty((est + 1024, 2), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for b in range(3):
+        ix.self_join_async(out, cnt, b, 3)
+    e.record()
+    torch.cuda.synchronize()
+    ts.append(s.elapsed_time(e))
+    ix.free()
+print(os.path.basename(os.path.dirname(pkg + "/")), "pairs", int(cnt.item()), "join ms", " ".join("%.1f" % t for t in ts))
