@@ -475,6 +475,7 @@ static int make_fp16(Index* ix, bool* ok) {
     // S: power of two with S * span in [90, 180]: r, h, R2 and the sentinel fit fp16
     ix->tc_scale = std::ldexp(1.0, (int)std::floor(std::log2(180.0 / span)));
     ix->k16 = (ix->n + 4 + 15) & ~15;
+    if (ix->k16 > 128) return GJ_OK;   // n > 124: no MMA depth instantiated; fall back to the SIMT filters
     const int64_t N = ix->N;
     // rows padded to a multiple of 8 plus one 256-row block of zeros: block loads
     // (<= 256 rows) that start at a row multiple of 8 never read past the allocation

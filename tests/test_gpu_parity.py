@@ -142,6 +142,19 @@ def test_certified_filters_near_the_boundary(rel, filt):
     check(D, eps, a)
 
 
+@pytest.mark.parametrize("dims", [124, 126, 128])
+def test_tensor_filters_at_the_dimension_limit(dims):
+    """n + 4 augmented columns must fit the largest MMA depth (128): n <= 124
+    runs the tcgen05 bound, n > 124 falls back to the FP32 / FP64 scan; pairs
+    exact either way."""
+    D = synth.exponential(1200, dims, seed=dims)
+    eps = 0.3
+    got, ix = gpu_pairs(D, eps, 4, filter=2)
+    assert (ix.info().filter == 2) == (dims <= 124)
+    check(D, eps, got)
+    assert len(got) > 1200
+
+
 @pytest.mark.parametrize("filt", [1, 2, 3])
 def test_filters_switch_off_when_they_cannot_certify(filt):
     # huge coordinate spread relative to eps: no certified filter is useful,
