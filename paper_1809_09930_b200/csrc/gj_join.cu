@@ -34,6 +34,8 @@
 namespace gj {
 namespace {
 
+constexpr int kWinRound = 256;   // adjacent cells whose windows are computed per round
+
 using Params = JoinParams;
 
 constexpr int kSmemDoubles = 4096;   // 32 KB candidate stage
@@ -63,7 +65,8 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     constexpr int TC = kSmemDoubles / NPR;   // candidates per shared-memory stage (even)
     __shared__ __align__(16) double Cs[kSmemDoubles];
     __shared__ uint32_t Cid[TC];
-    __shared__ uint32_t s_win[2];
+    __shared__ uint32_t s_wr[kWinRound], s_ws[kWinRound];   // SORTIDU windows of one round of adjacent cells
+    __shared__ unsigned char s_dg[kWinRound];
     __shared__ unsigned long long s_red[6][kTileQ / 32];
 
     const int tid = threadIdx.x, lane = tid & 31;
@@ -112,32 +115,45 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
     }
 
     const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
-    for (uint32_t b = nb0; b < nb1; ++b) {
-        const uint32_t B = P.nbr[b];
+    // SORTIDU windows of up to kWinRound adjacent cells at a time, one thread per
+    // cell (the binary searches run in parallel instead of one cell after another)
+    for (uint32_t w0 = nb0; w0 < nb1; w0 += kWinRound) {
+    const uint32_t nwin = min((uint32_t)kWinRound, nb1 - w0);
+    __syncthreads();   // the previous round's windows are no longer read
+    for (uint32_t i = tid; i < nwin; i += kTileQ) {
+        const uint32_t B = P.nbr[w0 + i];
         uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
-        if (P.sortidu) {   // tile-level SORTIDU window: union of the queries' u-windows
-            __syncthreads();
-            if (tid < 2) {   // tid 0: first r with u_lo - r(u) <= eps; tid 1: first s with s(u) - u_hi > eps
-                uint32_t lo = r, hi = s;
-                while (lo < hi) {
-                    uint32_t mid = (lo + hi) >> 1;
-                    double cu = P.pts[(size_t)mid * n_pad + P.u];
-                    bool pred = tid == 0 ? (u_lo - cu <= eps) : (cu - u_hi > eps);
-                    if (pred) hi = mid; else lo = mid + 1;
-                }
-                s_win[tid] = lo;
+        if (P.sortidu) {   // tile-level SORTIDU window (exact predicates on the fp64 u-coordinates)
+            uint32_t lo = r, hi = s;
+            while (lo < hi) {   // first r with u_lo - r(u) <= eps
+                const uint32_t mid = (lo + hi) >> 1;
+                if (u_lo - P.pts[(size_t)mid * n_pad + P.u] <= eps) hi = mid; else lo = mid + 1;
             }
-            __syncthreads();
-            r = s_win[0];
-            s = max(s_win[1], r);
+            const uint32_t rr = lo;
+            lo = r;
+            hi = s;
+            while (lo < hi) {   // first s with s(u) - u_hi > eps
+                const uint32_t mid = (lo + hi) >> 1;
+                if (P.pts[(size_t)mid * n_pad + P.u] - u_hi > eps) hi = mid; else lo = mid + 1;
+            }
+            r = rr;
+            s = max(lo, r);
         }
         const bool diag = SYM && B == g;
-        if (diag) r = max(r, q0 + 1);   // own cell: only candidates after the query
+        if (diag) r = max(r, q0 + 1);
         if (split > 1 && s > r) {
             const uint64_t len = s - r;
             s = r + (uint32_t)(len * (part + 1) / split);
             r = r + (uint32_t)(len * part / split);
         }
+        s_wr[i] = r;
+        s_ws[i] = max(s, r);
+        s_dg[i] = diag ? 1 : 0;
+    }
+    __syncthreads();
+    for (uint32_t wi = 0; wi < nwin; ++wi) {
+        const uint32_t r = s_wr[wi], s = s_ws[wi];
+        const bool diag = s_dg[wi] != 0;
         for (uint32_t cb = r; cb < s; cb += TC) {
             const int cntc = (int)min((uint32_t)TC, s - cb);
             __syncthreads();
@@ -234,6 +250,7 @@ __global__ void __launch_bounds__(kTileQ) k_join(Params P, JoinArgs A) {
                 }
             }
         }
+    }
     }
     if (MODE != kEmit) {
         if (MODE == kStats && !SYM) {
