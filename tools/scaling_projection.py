@@ -1,0 +1,56 @@
+"""Per-rank device time of one bench step for world = 1, 2, 4, 8, every rank's
+share run one after another on ONE GPU (index build, estimator, join of the
+rank's tiles), to project entity-partitioned scaling before 8 GPUs are
+available: python tools/scaling_projection.py [--workload expo32]
+The projection is max over ranks of (build + estimate + join); NCCL broadcast
+and all-reduce are not included (measured separately on NVLink)."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1809_09930_b200 import Index, num_batches  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--workload", default="expo32")
+p.add_argument("--reps", type=int, default=3)
+a = p.parse_args()
+w = synth.WORKLOADS[a.workload]
+D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+res = {}
+for world in (1, 2, 4, 8):
+    per_rank = []
+    for rank in range(world):
+        best = None
+        for _ in range(a.reps):
+            ev[0].record()
+            ix = Index(D, w["eps"], w["k"])
+            ev[1].record()
+            est = ix.estimate(0.01, rank, world)
+            ev[2].record()
+            nb = num_batches(est, 0)
+            cap = est * 2 + (1 << 20)
+            out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            for b in range(nb):
+                ix.self_join_async(out, cnt, b, nb, rank, world)
+            ev[3].record()
+            torch.cuda.synchronize()
+            t = [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
+            ix.free()
+            del out
+            if best is None or sum(t) < sum(best):
+                best = t
+        per_rank.append(best)
+    step = max(sum(t) for t in per_rank)
+    res[world] = {"step_ms": step, "per_rank_ms": per_rank}
+    eff = res[1]["step_ms"] / (world * step)
+    print(f"world {world}: max-over-ranks step {step:.1f} ms (build {per_rank[0][0]:.1f}, estimate {per_rank[0][1]:.1f}, "
+          f"join {max(t[2] for t in per_rank):.1f} max / {min(t[2] for t in per_rank):.1f} min) -> efficiency {eff:.2f}",
+          flush=True)
+print(json.dumps({"workload": a.workload, "projection": res}))
