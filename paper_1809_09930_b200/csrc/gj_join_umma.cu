@@ -11,6 +11,8 @@
 // bound iff its accumulator is > +0, and survivors are decided in FP64.
 #include <stdlib.h>
 
+#include <string>
+
 #include "gj_internal.cuh"
 #include "gj_umma.cuh"
 
@@ -84,13 +86,17 @@ constexpr int ws_warps() { return 2 + 4 * MT * EPW; }   // 0 producer, 1 MMA iss
 // CTAs per SM: two when a CTA's accumulator slots (MT x SL x BN columns) fit
 // in half of the SM's 512 TMEM columns.
 template <int BN, int MT, int SL>
-constexpr int ws_ctas_per_sm() { return MT * SL * BN <= 256 ? 2 : 1; }
+constexpr int ws_ctas_per_sm() { return MT * SL * BN <= 128 ? 4 : (MT * SL * BN <= 256 ? 2 : 1); }
+template <int BN, int MT, int SL>
+constexpr int ws_budget_kb() {
+    return ws_ctas_per_sm<BN, MT, SL>() == 4 ? 40 : (ws_ctas_per_sm<BN, MT, SL>() == 2 ? 96 : 196);
+}
 // Candidate ring depth: as many BN-row blocks as fit beside the A tiles in
 // ~100 KB (two CTAs per SM) or ~200 KB (one) of shared memory, at most 24.
 template <int KP, int BN, int MT, int SL>
 constexpr int ws_stages() {
-    return ((ws_ctas_per_sm<BN, MT, SL>() == 2 ? 96 : 196) * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
-               ? ((ws_ctas_per_sm<BN, MT, SL>() == 2 ? 96 : 196) * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
+    return (ws_budget_kb<BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
+               ? (ws_budget_kb<BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
                : 24;
 }
 
@@ -129,7 +135,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
     constexpr int NW = ws_warps<MT, EPW>();
     constexpr int NT = 32 * NW;
     constexpr int QT = kM * MT;            // queries per CTA
-    constexpr uint32_t TCOLS = MT * SL * BN <= 256 ? 256 : 512;   // TMEM columns allocated (power of 2)
+    constexpr uint32_t TCOLS = MT * SL * BN <= 128 ? 128 : (MT * SL * BN <= 256 ? 256 : 512);   // TMEM columns (power of 2)
     constexpr int KS = KP / 16;
     constexpr int ST = ws_stages<KP, BN, MT, SL>();
     constexpr int NACC = SL;
@@ -139,6 +145,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, M
     constexpr uint32_t kSBO = KP * 16;
     constexpr uint32_t kBlockBytes = BN * KP * 2;
     static_assert(NL >= 1 && NL <= 8, "epilogue columns per warp");
+    static_assert(ws_stages<KP, BN, MT, SL>() >= 1, "candidate ring needs at least one stage");
     // TMEM loads in flight per wait: 4 (128 columns) when one warp reads a whole
     // 256-column row (EPW = 1, 170 registers at two CTAs per SM), else 2
     constexpr int NC = NL >= 8 ? 4 : (NL < 2 ? NL : 2);
@@ -462,7 +469,8 @@ int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
     using Smem = WsSmem<KP, BN, MT, SL, EPW>;
     // two CTAs per SM (2 x 256 TMEM columns) or exactly one (512 columns),
     // forced by > 114 KB of shared memory
-    const size_t smem = std::max<size_t>(sizeof(Smem), ws_ctas_per_sm<BN, MT, SL>() == 2 ? 80 * 1024 : 120 * 1024);
+    constexpr int kCtas = ws_ctas_per_sm<BN, MT, SL>();
+    const size_t smem = std::max<size_t>(sizeof(Smem), kCtas == 4 ? 40 * 1024 : (kCtas == 2 ? 80 * 1024 : 120 * 1024));
     static_assert(sizeof(Smem) <= 227 * 1024 / ws_ctas_per_sm<BN, MT, SL>() - 1024, "shared memory");
     static bool attr_done = false;
     if (!attr_done) {
@@ -486,18 +494,23 @@ int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym,
                : launch_umma_k<KP, BN, MT, SL, EPW, kCount, false>(p, a, s);
 }
 
-template <int BN, int MT, int SL, int EPW>
+// MMA depth dispatch; KMAX bounds the instantiated depths (a configuration
+// whose shared memory cannot hold a deeper ring is not instantiated beyond it).
+template <int BN, int MT, int SL, int EPW, int KMAX = 128>
 int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     switch (ix->k16) {
         case 16: return launch_umma<16, BN, MT, SL, EPW>(p, mode, a, sym, s);
         case 32: return launch_umma<32, BN, MT, SL, EPW>(p, mode, a, sym, s);
         case 48: return launch_umma<48, BN, MT, SL, EPW>(p, mode, a, sym, s);
-        case 64: return launch_umma<64, BN, MT, SL, EPW>(p, mode, a, sym, s);
-        case 80: return launch_umma<80, BN, MT, SL, EPW>(p, mode, a, sym, s);
-        case 96: return launch_umma<96, BN, MT, SL, EPW>(p, mode, a, sym, s);
-        case 112: return launch_umma<112, BN, MT, SL, EPW>(p, mode, a, sym, s);
-        default: return launch_umma<128, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 64: if constexpr (KMAX >= 64) return launch_umma<64, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 80: if constexpr (KMAX >= 80) return launch_umma<80, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 96: if constexpr (KMAX >= 96) return launch_umma<96, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 112: if constexpr (KMAX >= 112) return launch_umma<112, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 128: if constexpr (KMAX >= 128) return launch_umma<128, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        default: break;
     }
+    set_error("tcgen05 join: MMA depth " + std::to_string(ix->k16) + " not instantiated for this configuration");
+    return GJ_ERR_INVALID;
 }
 
 }  // namespace
@@ -505,18 +518,28 @@ int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const Jo
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     const JoinParams p = join_params(ix);
     const bool sym = ix->opt.symmetric != 0;
-    // A tiles per CTA = tile_q / 128.  MT = 1 (default): 256-candidate blocks
-    // (UMMA N = 256: the issue loop's barrier handshakes are amortised over 384
-    // tensor cycles, tools/micro/umma_issue), one 256-column slot per CTA and
-    // two CTAs per SM (each CTA's epilogue overlaps the other's MMA), 8
-    // epilogue warps per CTA.  Timing comparisons: GJ_UMMA_CFG=2 (128-candidate
-    // blocks, two slots per CTA, two CTAs per SM), GJ_UMMA_CFG=3 (256-candidate
-    // blocks, two slots, one CTA per SM with 16 epilogue warps).
+    // A tiles per CTA = tile_q / 128.  MT = 1 (default): 128-candidate blocks,
+    // one 128-column accumulator per CTA and FOUR CTAs per SM (4 x 128 TMEM
+    // columns): four independent MMA -> epilogue pipelines per SM, so one CTA's
+    // epilogue (4 warps, 128 columns each) overlaps three others' MMAs.
+    // Timing comparisons (DESIGN "What bounds the tcgen05 join"):
+    // GJ_UMMA_CFG=1: 256-candidate blocks, two CTAs per SM, 8 epilogue warps;
+    // =2: 128-candidate blocks, two slots per CTA, two CTAs per SM;
+    // =3: 256-candidate blocks, two slots, one CTA per SM, 16 epilogue warps;
+    // =4: 256-candidate blocks, two CTAs per SM, one warp per row quarter.
     static const int cfg = [] { const char* e = getenv("GJ_UMMA_CFG"); return e ? atoi(e) : 0; }();
     if (ix->tile_q / kM == 2) return launch_umma_kp<128, 2, 2, 1>(ix, p, mode, a, sym, s);
-    if (cfg == 2) return launch_umma_kp<128, 1, 2, 2>(ix, p, mode, a, sym, s);
-    if (cfg == 4) return launch_umma_kp<256, 1, 1, 1>(ix, p, mode, a, sym, s);
-    if (cfg == 3) return launch_umma_kp<256, 1, 2, 4>(ix, p, mode, a, sym, s);
+    if (ix->k16 <= 64) {   // timing comparisons
+        if (cfg == 1) return launch_umma_kp<256, 1, 1, 2, 64>(ix, p, mode, a, sym, s);
+        if (cfg == 2) return launch_umma_kp<128, 1, 2, 2, 64>(ix, p, mode, a, sym, s);
+        if (cfg == 3) return launch_umma_kp<256, 1, 2, 4, 64>(ix, p, mode, a, sym, s);
+        if (cfg == 4) return launch_umma_kp<256, 1, 1, 1, 64>(ix, p, mode, a, sym, s);
+    }
+    // four CTAs per SM while A + two ring stages fit a quarter of the SM's
+    // shared memory (K <= 48); deeper rows: 256-candidate blocks with two CTAs
+    // per SM (measured on expo64_10m, K = 80: 10.9-11.1 s vs 11.6 s with
+    // 128-candidate blocks and two slots)
+    if (ix->k16 <= 48) return launch_umma_kp<128, 1, 1, 1, 48>(ix, p, mode, a, sym, s);
     return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
 }
 
