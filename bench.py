@@ -232,6 +232,9 @@ def main():
             else:
                 dist.barrier()
 
+    batch_streams = [torch.cuda.Stream() for _ in range(3)]
+    batch_done = [torch.cuda.Event() for _ in range(3)]
+
     def one_step(out, cnt, ev_join, ev_phase=None):
         """The timed hot path; returns (index, n_b).  ev_join brackets the join
         kernels; ev_phase (optional) = [after broadcast, after build, after estimate]."""
@@ -248,8 +251,14 @@ def main():
         nb = num_batches(est, args.batch_size)
         cnt.zero_()
         ev_join[0].record(stream)
+        # Fig. 4: batches on three streams, so one batch's tail overlaps the next
+        for i, bs in enumerate(batch_streams):
+            bs.wait_event(ev_join[0])
         for b in range(nb):
-            ix.self_join_async(out, cnt, b, nb, rank, world)
+            ix.self_join_async(out, cnt, b, nb, rank, world, stream=batch_streams[b % 3].cuda_stream)
+        for bs, be in zip(batch_streams, batch_done):
+            be.record(bs)
+            stream.wait_event(be)
         ev_join[1].record(stream)
         if world > 1:
             tot = cnt.clone()

@@ -190,6 +190,15 @@ GJ_API int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t ba
 GJ_API int gj_self_join_async(gj_index* idx, uint32_t* out_pairs, int64_t capacity, uint64_t* d_count,
                        int32_t batch, int32_t n_batches, int32_t rank, int32_t world);
 
+/* gj_self_join_async on a caller-chosen CUDA stream (0 = the index's stream)
+ * [async]: batches on different streams run concurrently (Fig. 4 uses three),
+ * so one batch's tail overlaps the next.  The caller orders `stream` after the
+ * index build (e.g. an event recorded on the index stream) and after the zeroing
+ * of *d_count; concurrent batches may share out_pairs and d_count. */
+GJ_API int gj_self_join_async_stream(gj_index* idx, uint32_t* out_pairs, int64_t capacity, uint64_t* d_count,
+                                     int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
+                                     uint64_t stream);
+
 /* Same, count only (no pair payload written) [async]. */
 GJ_API int gj_self_join_count_async(gj_index* idx, uint64_t* d_count, int32_t batch, int32_t n_batches,
                              int32_t rank, int32_t world);

@@ -309,6 +309,19 @@ int gj_self_join_async(gj_index* h, uint32_t* out_pairs, int64_t capacity, uint6
     return launch_join(&h->ix, kEmit, a, h->ix.stream);
 }
 
+int gj_self_join_async_stream(gj_index* h, uint32_t* out_pairs, int64_t capacity, uint64_t* d_count, int32_t batch,
+                              int32_t n_batches, int32_t rank, int32_t world, uint64_t stream) {
+    if (!h || !d_count || (capacity > 0 && !out_pairs) || capacity < 0) { set_error("bad argument"); return GJ_ERR_INVALID; }
+    if (int rc = check_rank(rank, world)) return rc;
+    if (n_batches < 1 || batch < 0 || batch >= n_batches) { set_error("need 0 <= batch < n_batches"); return GJ_ERR_INVALID; }
+    JoinArgs a{};
+    a.out = out_pairs;
+    a.cap = (uint64_t)capacity;
+    a.count = d_count;
+    batch_tiles(&h->ix, batch, n_batches, rank, world, &a);
+    return launch_join(&h->ix, kEmit, a, stream ? (cudaStream_t)stream : h->ix.stream);
+}
+
 int gj_self_join_count_async(gj_index* h, uint64_t* d_count, int32_t batch, int32_t n_batches, int32_t rank,
                              int32_t world) {
     if (!h || !d_count) { set_error("bad argument"); return GJ_ERR_INVALID; }

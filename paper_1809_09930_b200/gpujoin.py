@@ -19,7 +19,7 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 
 # Every symbol include/gpujoin.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
-           "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_fp32_accept_threshold", "gj_tc_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_count_async", "gj_self_join",
+           "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_fp32_accept_threshold", "gj_tc_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_async_stream", "gj_self_join_count_async", "gj_self_join",
            "gj_self_join_host", "gj_join_stats", "gj_join_counts", "gj_neighbor_table", "gj_free_index", "gj_last_error",
            "gj_abi_version", "gj_launch_count", "gj_release_cached_memory"]
 
@@ -75,6 +75,7 @@ def lib():
         "gj_fp32_accept_threshold": (C.c_int, [D, I32, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
         "gj_partition": (C.c_int, [I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
         "gj_self_join_async": (C.c_int, [P, P, I64, P, I32, I32, I32, I32]),
+        "gj_self_join_async_stream": (C.c_int, [P, P, I64, P, I32, I32, I32, I32, U64]),
         "gj_self_join_count_async": (C.c_int, [P, P, I32, I32, I32, I32]),
         "gj_self_join": (C.c_int, [P, P, I64, I32, I32, C.POINTER(I64)]),
         "gj_self_join_host": (C.c_int, [P, P, I64, I32, I32, I64, C.POINTER(I64), C.POINTER(C.c_int32)]),
@@ -182,12 +183,17 @@ class Index:
         _check(lib().gj_estimate(self._h, float(frac), rank, world, C.byref(e)))
         return e.value
 
-    def self_join_async(self, out_pairs, count, batch=0, n_batches=1, rank=0, world=1):
+    def self_join_async(self, out_pairs, count, batch=0, n_batches=1, rank=0, world=1, stream=None):
         """Enqueue one batch into device tensors out_pairs (uint32 [cap, 2] as
-        int32/uint32 tensor) and count (uint64/int64 device scalar)."""
+        int32/uint32 tensor) and count (uint64/int64 device scalar); on the
+        index's stream, or on `stream` (a cudaStream_t handle, gj_self_join_async_stream)."""
         cap = out_pairs.shape[0] if out_pairs is not None else 0
-        _check(lib().gj_self_join_async(self._h, _ptr(out_pairs) if cap else None, cap, _ptr(count), batch,
-                                        n_batches, rank, world))
+        if stream is None:
+            _check(lib().gj_self_join_async(self._h, _ptr(out_pairs) if cap else None, cap, _ptr(count), batch,
+                                            n_batches, rank, world))
+        else:
+            _check(lib().gj_self_join_async_stream(self._h, _ptr(out_pairs) if cap else None, cap, _ptr(count),
+                                                   batch, n_batches, rank, world, int(stream)))
 
     def self_join_count_async(self, count, batch=0, n_batches=1, rank=0, world=1):
         _check(lib().gj_self_join_count_async(self._h, _ptr(count), batch, n_batches, rank, world))

@@ -22,6 +22,7 @@ a = p.parse_args()
 w = synth.WORKLOADS[a.workload]
 D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+batch_streams = [torch.cuda.Stream() for _ in range(3)]   # as bench.py: three batch streams
 res = {}
 for world in (1, 2, 4, 8):
     per_rank = []
@@ -37,8 +38,16 @@ for world in (1, 2, 4, 8):
             cap = est * 2 + (1 << 20)
             out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
             cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            start = torch.cuda.Event()
+            start.record()
+            for bs in batch_streams:
+                bs.wait_event(start)
             for b in range(nb):
-                ix.self_join_async(out, cnt, b, nb, rank, world)
+                ix.self_join_async(out, cnt, b, nb, rank, world, stream=batch_streams[b % 3].cuda_stream)
+            for bs in batch_streams:
+                done = torch.cuda.Event()
+                done.record(bs)
+                torch.cuda.current_stream().wait_event(done)
             ev[3].record()
             torch.cuda.synchronize()
             t = [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
