@@ -52,13 +52,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+// The suspend-time hint lets a waiting thread sleep in hardware until the
+// phase completes (or the hint expires) instead of re-polling: the join's
+// role warps otherwise spend billions of issue slots per launch spinning.
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
-        "r"(parity));
+        "r"(parity), "r"(0x989680u));
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
