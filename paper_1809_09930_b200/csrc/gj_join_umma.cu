@@ -85,18 +85,22 @@ template <int MT, int EPW>
 constexpr int ws_warps() { return 2 + 4 * MT * EPW; }   // 0 producer, 1 MMA issuer, epilogue
 // CTAs per SM: two when a CTA's accumulator slots (MT x SL x BN columns) fit
 // in half of the SM's 512 TMEM columns.
-template <int BN, int MT, int SL>
-constexpr int ws_ctas_per_sm() { return MT * SL * BN <= 128 ? 4 : (MT * SL * BN <= 256 ? 2 : 1); }
-template <int BN, int MT, int SL>
+// (128-column accumulators: four CTAs per SM up to K = 48, three beyond, where
+// A + two ring stages no longer fit a quarter of the shared memory)
+template <int KP, int BN, int MT, int SL>
+constexpr int ws_ctas_per_sm() { return MT * SL * BN <= 128 ? (KP <= 48 ? 4 : 3) : (MT * SL * BN <= 256 ? 2 : 1); }
+template <int KP, int BN, int MT, int SL>
 constexpr int ws_budget_kb() {
-    return ws_ctas_per_sm<BN, MT, SL>() == 4 ? 40 : (ws_ctas_per_sm<BN, MT, SL>() == 2 ? 96 : 196);
+    return ws_ctas_per_sm<KP, BN, MT, SL>() == 4 ? 40
+           : ws_ctas_per_sm<KP, BN, MT, SL>() == 3 ? 64
+           : (ws_ctas_per_sm<KP, BN, MT, SL>() == 2 ? 96 : 196);
 }
 // Candidate ring depth: as many BN-row blocks as fit beside the A tiles in
 // ~100 KB (two CTAs per SM) or ~200 KB (one) of shared memory, at most 24.
 template <int KP, int BN, int MT, int SL>
 constexpr int ws_stages() {
-    return (ws_budget_kb<BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
-               ? (ws_budget_kb<BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
+    return (ws_budget_kb<KP, BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
+               ? (ws_budget_kb<KP, BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
                : 24;
 }
 
@@ -127,7 +131,7 @@ struct WsSmem {
 //               whose candidate lies in [r, s) (and after the query in its own
 //               cell) for a lane-parallel FP64 decision.
 template <int KP, int BN, int MT, int SL, int EPW, int MODE, bool SYM>
-__global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<BN, MT, SL>())
+__global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, BN, MT, SL>())
     k_join_umma(JoinParams P, JoinArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WsSmem<KP, BN, MT, SL, EPW>& S = *reinterpret_cast<WsSmem<KP, BN, MT, SL, EPW>*>(smem_raw);
@@ -469,9 +473,11 @@ int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
     using Smem = WsSmem<KP, BN, MT, SL, EPW>;
     // two CTAs per SM (2 x 256 TMEM columns) or exactly one (512 columns),
     // forced by > 114 KB of shared memory
-    constexpr int kCtas = ws_ctas_per_sm<BN, MT, SL>();
-    const size_t smem = std::max<size_t>(sizeof(Smem), kCtas == 4 ? 40 * 1024 : (kCtas == 2 ? 80 * 1024 : 120 * 1024));
-    static_assert(sizeof(Smem) <= 227 * 1024 / ws_ctas_per_sm<BN, MT, SL>() - 1024, "shared memory");
+    constexpr int kCtas = ws_ctas_per_sm<KP, BN, MT, SL>();
+    const size_t smem = std::max<size_t>(sizeof(Smem), kCtas == 4 ? 40 * 1024
+                                                        : kCtas == 3 ? 58 * 1024
+                                                        : (kCtas == 2 ? 80 * 1024 : 120 * 1024));
+    static_assert(sizeof(Smem) <= 227 * 1024 / ws_ctas_per_sm<KP, BN, MT, SL>() - 1024, "shared memory");
     static bool attr_done = false;
     if (!attr_done) {
         GJ_CUDA(cudaFuncSetAttribute((const void*)k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM>,
@@ -535,11 +541,13 @@ int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStre
         if (cfg == 3) return launch_umma_kp<256, 1, 2, 4, 64>(ix, p, mode, a, sym, s);
         if (cfg == 4) return launch_umma_kp<256, 1, 1, 1, 64>(ix, p, mode, a, sym, s);
     }
-    // four CTAs per SM while A + two ring stages fit a quarter of the SM's
-    // shared memory (K <= 48); deeper rows: 256-candidate blocks with two CTAs
-    // per SM (measured on expo64_10m, K = 80: 10.9-11.1 s vs 11.6 s with
-    // 128-candidate blocks and two slots)
+    // 128-candidate blocks with one accumulator per CTA: four CTAs per SM while
+    // A + two ring stages fit a quarter of the SM's shared memory (K <= 48),
+    // three up to K = 96 (3M x 64-d exponential, K = 80: 885 vs 899 ms with
+    // 256-candidate blocks and two CTAs per SM); K = 112, 128: 256-candidate
+    // blocks, two CTAs per SM
     if (ix->k16 <= 48) return launch_umma_kp<128, 1, 1, 1, 48>(ix, p, mode, a, sym, s);
+    if (ix->k16 <= 96) return launch_umma_kp<128, 1, 1, 1, 96>(ix, p, mode, a, sym, s);
     return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
 }
 

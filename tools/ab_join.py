@@ -7,7 +7,9 @@ sys.path.insert(1, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import synth
 from paper_1809_09930_b200 import Index
-w = synth.WORKLOADS["expo32"]
+w = dict(synth.WORKLOADS[os.environ.get("AB_WORKLOAD", "expo32")])
+if os.environ.get("AB_COUNT"):
+    w["count"] = int(os.environ["AB_COUNT"])
 D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
 import paper_1809_09930_b200 as P
 assert P.__file__.startswith(pkg), P.__file__
