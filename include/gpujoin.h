@@ -166,8 +166,9 @@ GJ_API int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t str
 
 /* computeNumBatches (§3.2.2 l.199-200): n_b = max(3, ceil(est / batch_size)).
  * batch_size <= 0 selects the device-memory-sized b_s (reading R15): a quarter of
- * the current device's free HBM split over the 3 pipeline result slots, 8 bytes
- * per pair (~1.9e9 pairs on an idle 180 GB B200), at least the paper's 1e8. */
+ * the current device's free HBM (sampled at the first such call in the process)
+ * split over the 3 pipeline result slots, 8 bytes per pair (~1.9e9 pairs on an
+ * idle 180 GB B200), at least the paper's 1e8. */
 GJ_API int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size);
 
 /* Entity partitioning arithmetic (§6.2 l.1013), host only: the tile positions

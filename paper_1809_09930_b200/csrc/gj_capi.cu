@@ -280,14 +280,26 @@ int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t stream) {
 
 // b_s sized against device memory (reading R15): the paper's 1e8 pairs was
 // sized for 2018 GPUs; a B200 holds ~2e10 pairs.
+// Sized once per device and process (cudaMemGetInfo is a driver round trip
+// that can stall the host for milliseconds; the join path calls this per step).
 static int64_t auto_batch_size() {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    static int64_t cached[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
         cudaGetLastError();
         return 100000000ll;
     }
-    const int64_t bs = (int64_t)(free_b / 4 / 3 / 8);
-    return std::max<int64_t>(100000000ll, bs);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!cached[dev]) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            return 100000000ll;
+        }
+        cached[dev] = std::max<int64_t>(100000000ll, (int64_t)(free_b / 4 / 3 / 8));
+    }
+    return cached[dev];
 }
 
 int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size) {
