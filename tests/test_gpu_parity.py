@@ -189,6 +189,19 @@ def test_degenerate_inputs():
     D[:, 2] = 0.0
     got, _ = gpu_pairs(D, 0.2, 3)
     check(D, 0.2, got)
+    # one dimension (k = n = 1); eps beyond the diameter (every ordered pair)
+    D = synth.uniform(500, 1, seed=4)
+    got, _ = gpu_pairs(D, 0.01, 1)
+    check(D, 0.01, got)
+    D = synth.uniform(700, 8, seed=5)
+    got, _ = gpu_pairs(D, 10.0, 4)
+    assert len(got) == 700 * 700
+    # a dense duplicate cluster inside scattered points: one very heavy tile
+    # (work-balanced split plans), for every filter
+    D = np.concatenate([np.tile(np.array([[0.41] * 10]), (400, 1)), synth.uniform(600, 10, seed=6)])
+    for filt in (0, 1, 2, 3):
+        got, ix = gpu_pairs(D, 0.3, 4, filter=filt)
+        check(D, 0.3, got)
 
 
 def test_index_structure_matches_algorithm1_oracle():
