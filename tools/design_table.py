@@ -25,7 +25,7 @@ out = [f"## Measured (1 B200, round 1; `{sys.argv[1]}`, `{sys.argv[2]}`)", "",
        "`bench.py --steps 3 --warmup 3` per line (the bench default line: 5 steps); step = index build + estimator + "
        "batched join, inputs resident in HBM; join = the join kernels of all result batches (CUDA events); e2e = the "
        "same through the C ABI from host memory (median step).  Roofline fraction: tensor = 2n x evaluated tests / "
-       "join time / 1389 TFLOP/s (measured bf16 sustained); alu = 3 flops x SHORTC dims / join time / derived FP32 or "
+       "join time / the bf16 sustained peak (bench `roofline.peak`, `peak_note`); alu = 3 flops x SHORTC dims / join time / derived FP32 or "
        "FP64 peak (DESIGN §Roofline).", "",
        "| workload | eps | k | flags | filter | n_b | pairs | S_D | join ms | step ms | pairs/s | e2e ms | roofline frac |",
        "|---|---|---|---|---|---|---|---|---|---|---|---|---|", row(b)] + [row(d) for d in rows]
