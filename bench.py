@@ -340,7 +340,7 @@ def main():
         host_out = torch.empty((cap, 2), dtype=torch.int32, pin_memory=True)
         e2e_s = []
         n_e2e_warm = max(3, args.warmup)   # first host builds grow the library's memory pool
-        for i in range(n_e2e_warm + max(3, args.steps)):
+        for i in range(n_e2e_warm + max(7, args.steps)):   # median of >= 7: robust to host-side outliers
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
