@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -50,6 +51,11 @@ cudaError_t pool_malloc_raw(void** p, size_t bytes, cudaStream_t s) {
     cudaMemPool_t pool;
     cudaError_t e = device_pool(&pool);
     if (e != cudaSuccess) return e;
+    // large requests in 32 MB granules: a freed block then fits the next step's
+    // request of a slightly different size (estimate-sized result batches)
+    // instead of fragmenting the cache and making the pool map new memory
+    constexpr size_t kGranule = 32ull << 20;
+    if (bytes > kGranule / 2) bytes = (bytes + kGranule - 1) / kGranule * kGranule;
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
@@ -183,18 +189,40 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     const double* dX = points;
     double* staged = nullptr;
     int rc = GJ_OK;
-    if (!is_device_ptr(points)) {
+    static const bool trace = getenv("GJ_TRACE") != nullptr;   // host-side phase times (diagnostics)
+    const auto ta = std::chrono::steady_clock::now();
+    auto ms_since = [](std::chrono::steady_clock::time_point t) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+    };
+    const bool on_device = is_device_ptr(points);
+    if (trace) fprintf(stderr, "[gj] build_index: pointer query %.1f ms\n", ms_since(ta));
+    if (!on_device) {
         size_t bytes = (size_t)n_points * dim * sizeof(double);
-        if (pool_malloc(&staged, bytes, ix.stream) != cudaSuccess) {
+        const auto tp = std::chrono::steady_clock::now();
+        const cudaError_t ea = pool_malloc(&staged, bytes, ix.stream);
+        if (trace) fprintf(stderr, "[gj] build_index: staging alloc %.1f ms\n", ms_since(tp));
+        if (ea != cudaSuccess) {
             cudaGetLastError();
             set_error("device allocation for staged points failed");
             delete h;
             return GJ_ERR_NOMEM;
         }
+        const auto tc = std::chrono::steady_clock::now();
         cudaMemcpyAsync(staged, points, bytes, cudaMemcpyHostToDevice, ix.stream);
+        if (trace) fprintf(stderr, "[gj] build_index: H2D enqueue %.1f ms\n", ms_since(tc));
         dX = staged;
     }
+    if (trace) {
+        const auto t0 = std::chrono::steady_clock::now();
+        cudaStreamSynchronize(ix.stream);
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[gj] build_index: staging + H2D %.1f ms\n", std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
+    const auto tb = std::chrono::steady_clock::now();
     rc = build_index(&ix, dX);
+    if (trace)
+        fprintf(stderr, "[gj] build_index: build %.1f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb).count());
     if (staged) cudaFreeAsync(staged, ix.stream);
     if (rc != GJ_OK) {
         gj_free_index(h);
