@@ -41,6 +41,19 @@ cudaError_t device_pool(cudaMemPool_t* out) {
         if ((e = cudaMemPoolCreate(&g_pool[dev], &props)) != cudaSuccess) return e;
         uint64_t keep = ~0ull;
         if ((e = cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) return e;
+        // warm the pool with one large reservation (1/16 of the free memory, at
+        // most 8 GB): later requests are carved from memory that is already
+        // mapped, instead of the pool growing (and the host stalling) mid-join
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const size_t want = std::min<size_t>(8ull << 30, free_b / 16);
+            void* tmp = nullptr;
+            if (want > 0 && cudaMallocFromPoolAsync(&tmp, want, g_pool[dev], 0) == cudaSuccess) {
+                cudaFreeAsync(tmp, 0);
+                cudaStreamSynchronize(0);
+            }
+            cudaGetLastError();
+        }
     }
     *out = g_pool[dev];
     return cudaSuccess;
