@@ -535,8 +535,8 @@ int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStre
     // =4: 256-candidate blocks, two CTAs per SM, one warp per row quarter.
     static const int cfg = [] { const char* e = getenv("GJ_UMMA_CFG"); return e ? atoi(e) : 0; }();
     if (ix->tile_q / kM == 2) return launch_umma_kp<128, 2, 2, 1>(ix, p, mode, a, sym, s);
+    if (cfg == 1) return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
     if (ix->k16 <= 64) {   // timing comparisons
-        if (cfg == 1) return launch_umma_kp<256, 1, 1, 2, 64>(ix, p, mode, a, sym, s);
         if (cfg == 2) return launch_umma_kp<128, 1, 2, 2, 64>(ix, p, mode, a, sym, s);
         if (cfg == 3) return launch_umma_kp<256, 1, 2, 4, 64>(ix, p, mode, a, sym, s);
         if (cfg == 4) return launch_umma_kp<256, 1, 1, 1, 64>(ix, p, mode, a, sym, s);
