@@ -291,29 +291,41 @@ __global__ void k_tile_count(const uint32_t* __restrict__ cell_start, int64_t G,
     if (g < G) nt[g] = (cell_start[g + 1] - cell_start[g] + tq - 1) / tq;
 }
 
+// One thread per TILE (a cell's tiles are consecutive from toff[g]; every
+// non-empty cell has at least one, so toff is strictly increasing): the few
+// huge cells of skewed data no longer serialise thousands of tiles on one thread.
 __global__ void k_tile_fill(const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ toff,
                             const uint64_t* __restrict__ cand, const uint64_t* __restrict__ cand_after, int sym,
-                            int64_t G, uint32_t tq, uint32_t* __restrict__ tile_cell,
+                            int64_t G, int64_t T, uint32_t tq, uint32_t* __restrict__ tile_cell,
                             uint32_t* __restrict__ tile_q0, uint64_t* __restrict__ tile_work,
                             uint64_t* __restrict__ sort_key, uint32_t* __restrict__ sort_val,
                             unsigned long long* __restrict__ total) {
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
-    uint32_t a = cell_start[g], b = cell_start[g + 1];
-    uint32_t t = toff[g];
-    for (uint32_t q = a; q < b; q += tq, ++t) {
-        uint32_t nq = min(tq, b - q);
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long tot = 0;
+    if (t < T) {
+        int64_t lo = 0, hi = G;   // last g with toff[g] <= t
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)toff[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int64_t g = lo;
+        const uint32_t a = cell_start[g], b = cell_start[g + 1];
+        const uint32_t q = a + (uint32_t)(t - (int64_t)toff[g]) * tq;
+        const uint32_t nq = min(tq, b - q);
         // candidate tests of the tile: all adjacent points per query, or (symmetric)
         // points of later cells plus the later points of the own cell
-        uint64_t w = sym ? (uint64_t)nq * (cand_after[g] + (b - q)) - (uint64_t)nq * (nq + 1) / 2
-                         : (uint64_t)nq * cand[g];
+        const uint64_t w = sym ? (uint64_t)nq * (cand_after[g] + (b - q)) - (uint64_t)nq * (nq + 1) / 2
+                               : (uint64_t)nq * cand[g];
         tile_cell[t] = (uint32_t)g;
         tile_q0[t] = q;
         tile_work[t] = w;
         sort_key[t] = ~w;   // descending work
-        sort_val[t] = t;
+        sort_val[t] = (uint32_t)t;
+        tot = (unsigned long long)nq * cand[g];   // queries x candidates (pre-SORTIDU) of the tile
     }
-    atomicAdd(total, (unsigned long long)((uint64_t)(b - a) * cand[g]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(total, tot);
 }
 
 int col_reduce(const double* X, int64_t m, int64_t rstride, int n, int mode, const double* mean, double* outa,
@@ -622,7 +634,7 @@ int build_index(Index* ix, const double* X) {
     unsigned long long* d_total = nullptr;
     GJ_CUDA(pool_malloc(&d_total, sizeof(*d_total), s));
     GJ_CUDA(cudaMemsetAsync(d_total, 0, sizeof(*d_total), s));
-    k_tile_fill<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, pos, cand, cand_after, ix->opt.symmetric, G,
+    k_tile_fill<<<blocks_for(T, 256), 256, 0, s>>>(ix->cell_start, pos, cand, cand_after, ix->opt.symmetric, G, T,
                                                    (uint32_t)ix->tile_q,
                                                    ix->tile_cell, ix->tile_q0,
                                                    ix->tile_work, skey, ix->tile_order, d_total); count_launch();
