@@ -21,7 +21,6 @@ Citations (PAPER.md line numbers):
   computeNumBatches §3.2.2 l.199-200 n_b >= 3, b_s
   selectivity       §5.2 l.800
   entity partition  §6.2 l.1013 "GPU p_k is assigned Q_l ... if l mod |p| = k"
-  k-cost model      §5.6 l.896 |D| 3^k log2|G| and mu (1/f)
   search loss       §4.1 l.252 l(n,k) = (3^n - 3^k)/3^n
 
 Readings (DESIGN.md §"Readings"): R2 grid edges on the eps-lattice through 0
@@ -236,10 +235,3 @@ def assign_query_sets(n_sets: int, n_gpus: int):
     if n_sets % n_gpus:
         raise ValueError("N_b mod |p| must be 0")
     return {g: [l for l in range(n_sets) if l % n_gpus == g] for g in range(n_gpus)}
-
-
-# ---------------------------------------------------- k selection (§5.6)
-def k_cost(n_points: int, k: int, n_nonempty: int, mu: float, f: float):
-    """§5.6 l.896: (search memory ops, comparison memory ops) =
-    (|D| 3^k log2|G|, mu / f)."""
-    return n_points * 3 ** k * math.log2(max(n_nonempty, 1)), mu / f

@@ -66,14 +66,66 @@ def test_sortidu_scan_example():
     assert grid.sortidu_window(u, -5.0, 0.1) == (0, 0)
 
 
-def test_entity_partition_and_k_cost():
+def test_entity_partition():
     a = grid.assign_query_sets(32, 4)
     assert a[0] == list(range(0, 32, 4)) and all(len(v) == 8 for v in a.values())
     assert grid.assign_query_sets(128, 16)[3] == list(range(3, 128, 16))
     with pytest.raises(ValueError):
         grid.assign_query_sets(30, 4)
-    s, c = grid.k_cost(1000, 3, 100, mu=5e5, f=0.01)
-    assert s == pytest.approx(1000 * 27 * math.log2(100)) and c == pytest.approx(5e7)
+
+
+def test_sortidu_window_ends_exactly_at_eps():
+    """§4.3 l.515-517: r is the first candidate with p(u) - r(u) <= eps (so a
+    candidate exactly eps below p(u) is inside) and the scan runs while
+    s(u) - p(u) <= eps (so a candidate exactly eps above is inside too); the
+    first candidate beyond eps on either side is outside.  Exact binary
+    fractions, so no rounding decides the ends."""
+    u = np.array([0.0, 0.25, 0.5, 0.75, 1.0, 1.25])
+    assert grid.sortidu_window(u, 0.75, 0.5) == (1, 6)      # 0.25 is 0.5 below: in; 1.25 0.5 above: in
+    assert grid.sortidu_window(u, 0.75, 0.25) == (2, 5)     # ends at 0.5 and 1.0, both exactly eps
+    assert grid.sortidu_window(u, 0.5, 0.0) == (2, 3)       # eps = 0: only the equal coordinate
+    assert grid.sortidu_window(u, 0.625, 0.125) == (2, 4)   # 0.5 and 0.75 exactly eps away
+
+
+def _exact_lattice_join(P, eps_int):
+    """Integer brute force (Python ints, no rounding): (i, j) with
+    sum_j (a_j - b_j)^2 <= eps^2 (§3.1 l.104-106, reading R3)."""
+    pts = [tuple(int(v) for v in row) for row in P]
+    e2 = eps_int * eps_int
+    return {(i, j) for i, a in enumerate(pts) for j, b in enumerate(pts)
+            if sum((x - y) ** 2 for x, y in zip(a, b)) <= e2}
+
+
+@pytest.mark.parametrize("dims,eps_int", [(4, 2), (5, 3)])
+def test_grid_join_exact_boundary_lattice(dims, eps_int):
+    """Integer lattice points with an integer eps: many pairs lie EXACTLY at
+    distance eps, many of them with |p(u) - c(u)| = eps on the SORTIDU dim
+    and 0 elsewhere.  The grid join must return exactly the integer
+    brute-force set for every k and flag combination -- a '<' for '<=' at
+    either SORTIDU end, at the SHORTC test or in the adjacency range fails."""
+    rng = np.random.default_rng(dims * 10 + eps_int)
+    P = rng.integers(0, 3 * eps_int + 1, size=(260, dims))
+    # for every dim d a pair differing by exactly eps in d only: whichever dim
+    # REORDER and k make the SORTIDU dim u, the exactly-at-eps window end occurs
+    base = np.full((1, dims), 1)
+    P = np.unique(np.concatenate([P, base, base + eps_int * np.eye(dims, dtype=np.int64)]), axis=0)
+    P = P.astype(np.float64)
+    exact = _exact_lattice_join(P, eps_int)
+    sure, amb = brute.self_join(P, float(eps_int))
+    assert as_set(sure) | as_set(amb) == exact                 # boundary pairs are in the band and inside
+    assert len(amb) >= 50                                     # many pairs exactly at eps
+    for k in range(1, dims + 1):
+        for reorder in (False, True):
+            for sortidu in (False, True):
+                P_out, _ = grid.gpu_join(P, float(eps_int), k, reorder, sortidu, shortc=True, frac=1.0)
+                assert as_set(P_out) == exact, (k, reorder, sortidu)
+    # the exactly-at-eps SORTIDU case is present: a pair differing by eps in u only
+    Dr, _ = grid.reorder_variance(P, 1.0)
+    G = grid.construct_index(Dr, float(eps_int), 1)
+    u = G["u"]
+    diff = np.abs(Dr[:, None, :] - Dr[None, :, :])
+    only_u = (diff[:, :, u] == eps_int) & (np.delete(diff, u, axis=2).sum(axis=2) == 0)
+    assert only_u.any()
 
 
 def test_linearize_roundtrip_is_bijective():
