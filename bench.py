@@ -65,8 +65,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stats", action="store_true",
                    help="skip the FP64 work-counter pass (roofline = null); for large sweep workloads")
-    p.add_argument("--cpu-sample", type=int, default=96,
-                   help="oracle query sample for cpu_baseline (~13 s on expo32; the reference arm uses a quarter per step)")
+    p.add_argument("--cpu-sample", type=int, default=None,
+                   help="oracle query sample for cpu_baseline / each reference-arm step (default 96: about "
+                        "14 s of CPU work on expo32, spread over all host cores)")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu baseline/clocks")
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo lets several ranks share one GPU "
                    "to exercise the multi-rank path on a 1-GPU box")
@@ -131,18 +132,67 @@ def workload(args):
     return w
 
 
+_POOL_D = None
+
+
+def _oracle_chunk(args):
+    """Worker: the oracle (oracle/brute.neighbors_of, unchanged) on a chunk of
+    query ids against the full dataset inherited from the parent (fork)."""
+    from oracle import brute
+    eps, q = args
+    t = time.perf_counter()
+    res = brute.neighbors_of(_POOL_D, eps, q)
+    return sum(len(s) + len(a) for s, a in res), time.perf_counter() - t
+
+
 def cpu_baseline(D, eps, m, seed):
     """The oracle as it stands (oracle/brute.neighbors_of), timed on a bounded
-    sample of m query points against the full dataset on the host."""
-    from oracle import brute
+    sample of m query points against the full dataset on ALL host cores: the
+    queries are split over one forked worker per core (numpy single-threaded
+    in each), wall-clock timed around the whole pool."""
+    import multiprocessing as mp
+    global _POOL_D
     q = synth.query_sample(D.shape[0], m, seed=seed + 1)
-    t = time.perf_counter()
-    res = brute.neighbors_of(D, eps, q)
-    dt = time.perf_counter() - t
-    pairs = sum(len(s) + len(a) for s, a in res)
-    return {"value": pairs / dt, "unit": "pairs/s", "cores": 1, "kind": "oracle",
-            "sample": f"{len(q)} query points x all {D.shape[0]} points (brute force, numpy einsum, 1 thread)",
-            "seconds": dt, "pairs": pairs}
+    cores = max(1, min(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count(), len(q)))
+    chunks = [q[i::cores] for i in range(cores)]
+    _POOL_D = D
+    env_threads = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_threads:
+        os.environ[k] = "1"
+    try:
+        ctx = mp.get_context("fork")
+        t = time.perf_counter()
+        with ctx.Pool(cores) as pool:
+            res = pool.map(_oracle_chunk, [(eps, c) for c in chunks])
+        dt = time.perf_counter() - t
+    finally:
+        _POOL_D = None
+        for k, v in env_threads.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    pairs = sum(r[0] for r in res)
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+            "sample": f"{len(q)} query points x all {D.shape[0]} points (brute force, numpy einsum; "
+                      f"queries split over {cores} forked workers, one per core)",
+            "seconds": dt, "cpu_seconds": float(sum(r[1] for r in res)), "pairs": pairs}
+
+
+def traffic_record(workload, filt):
+    """The newest profiles/*_join_traffic_<workload>.json (tools/ncu_join_traffic.py)
+    for the kernel of this filter, or None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_join_traffic_{workload}.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        if d.get("filter", 2) == filt:
+            d["source"] = os.path.relpath(f, ROOT)
+            best = d
+    return best
 
 
 def run_reference(args):
@@ -152,9 +202,10 @@ def run_reference(args):
         return
     w = workload(args)
     D = synth.make(w["gen"], w["count"], w["dims"], seed=args.seed)
-    times, pairs = [], 0
+    times, pairs, cores = [], 0, 1
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(D, w["eps"], max(1, args.cpu_sample // 4), args.seed + i)
+        cb = cpu_baseline(D, w["eps"], args.cpu_sample, args.seed + i)
+        cores = cb["cores"]
         if i >= args.warmup:
             times.append(cb["seconds"])
             pairs += cb["pairs"]
@@ -164,14 +215,16 @@ def run_reference(args):
             "ms_per_step": 1000 * float(np.mean(times)), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, **{k: w[k] for k in ("count", "dims", "eps", "k")}},
-            "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{max(1, args.cpu_sample // 4)} query points per step x all points"},
+            "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.cpu_sample} query points per step x all points, over {cores} cores"},
             "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
+    if args.cpu_sample is None:
+        args.cpu_sample = 96
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -179,7 +232,8 @@ def main():
 
     import __graft_entry__
     __graft_entry__.build()
-    from paper_1809_09930_b200 import Index, gpujoin, num_batches
+    from paper_1809_09930_b200 import Index, gpujoin
+    from paper_1809_09930_b200.distributed import Comm, EntityPartitionedJoin
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -192,6 +246,8 @@ def main():
         else:
             dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
+    comm = Comm(device=dev)
+    assert (comm.rank, comm.world) == (rank, world)
     stream = torch.cuda.current_stream()
     w = workload(args)
     flags = dict(reorder=not args.no_reorder, sortidu=not args.no_sortidu, shortc=not args.no_shortc,
@@ -207,87 +263,32 @@ def main():
     if rank == 0:
         D_dev.copy_(torch.from_numpy(D_host))
 
-    def bcast(t):
-        """NCCL broadcast over NVLink; with --dist-backend gloo staged through host memory."""
-        if args.dist_backend == "nccl":
-            dist.broadcast(t, src=0)
-        else:
-            h = t.cpu()
-            dist.broadcast(h, src=0)
-            t.copy_(h)
-
-    def allreduce(t, op=None):
-        op = op or dist.ReduceOp.SUM
-        if args.dist_backend == "nccl":
-            dist.all_reduce(t, op=op)
-        else:
-            h = t.cpu()
-            dist.all_reduce(h, op=op)
-            t.copy_(h)
-
-    def barrier():
-        if world > 1:
-            if args.dist_backend == "nccl":
-                dist.barrier(device_ids=[local])
-            else:
-                dist.barrier()
-
-    batch_streams = [torch.cuda.Stream() for _ in range(3)]
-    batch_done = [torch.cuda.Event() for _ in range(3)]
-
-    def one_step(out, cnt, ev_join, ev_phase=None):
-        """The timed hot path; returns (index, n_b).  ev_join brackets the join
-        kernels; ev_phase (optional) = [after broadcast, after build, after estimate]."""
-        if world > 1:
-            bcast(D_dev)
-        if ev_phase:
-            ev_phase[0].record(stream)
-        ix = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
-        if ev_phase:
-            ev_phase[1].record(stream)
-        est = ix.estimate(0.01, rank, world)
-        if ev_phase:
-            ev_phase[2].record(stream)
-        nb = num_batches(est, args.batch_size)
-        cnt.zero_()
-        ev_join[0].record(stream)
-        # Fig. 4: batches on three streams, so one batch's tail overlaps the next
-        for i, bs in enumerate(batch_streams):
-            bs.wait_event(ev_join[0])
-        for b in range(nb):
-            ix.self_join_async(out, cnt, b, nb, rank, world, stream=batch_streams[b % 3].cuda_stream)
-        for bs, be in zip(batch_streams, batch_done):
-            be.record(bs)
-            stream.wait_event(be)
-        ev_join[1].record(stream)
-        if world > 1:
-            tot = cnt.clone()
-            allreduce(tot)
-        return ix, nb
-
     # ---- capacity: exact count of this rank's share (outside any timed region)
-    if world > 1:
-        bcast(D_dev)
+    comm.broadcast(D_dev)
     ix0 = Index(D_dev, w["eps"], w["k"], stream=stream.cuda_stream, **flags)
     info = ix0.info()
     exact = ix0.estimate(1.0, rank, world)
     # work counters for the roofline: the tensor-core filters' unit is the
     # evaluated test (gj_join_counts, no distance work); the SHORTC scans need the
     # per-dimension counts of the FP64 stats scan (gj_join_stats)
-    stats = None
+    stats, mma_tests = None, None
     if not (args.profile or args.no_stats):
         stats = ix0.counts(rank, world) if info.filter in (2, 3) else ix0.stats(rank, world)
+        if info.filter == 2:
+            mma_tests = ix0.mma_tests(rank, world) * (world if world > 1 else 1)
+    info_k16 = info.mma_depth or None
     ix0.free()
     cap = int(exact * 1.02) + 65536
     out = torch.empty((cap, 2), dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    job = EntityPartitionedJoin(comm, D_dev, w["eps"], w["k"], out, cnt, args.batch_size, stream, **flags)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     # L2 hygiene: the point array (N*n*8 bytes) and the index are re-built every
     # step; an extra 256 MB flush buffer is written between timed steps.
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
     for _ in range(args.warmup):
-        ix, nb = one_step(out, cnt, ev[2:4])
+        ix, nb, _ = job.step(ev[2:4])
         torch.cuda.synchronize()
         ix.free()
     launches0 = gpujoin.launch_count()
@@ -295,13 +296,13 @@ def main():
     step_ms, join_ms, phase_ms, pairs = [], [], [], 0
     for _ in range(args.steps):
         flush.fill_(1)
-        barrier()
+        comm.barrier()
         torch.cuda.synchronize()
         ev[0].record(stream)
-        ix, nb = one_step(out, cnt, ev[2:4], ev[4:7])
+        ix, nb, _ = job.step(ev[2:4], ev[4:7])
         ev[1].record(stream)
         torch.cuda.synchronize()
-        barrier()
+        comm.barrier()
         step_ms.append(ev[0].elapsed_time(ev[1]))
         join_ms.append(ev[2].elapsed_time(ev[3]))
         phase_ms.append([ev[0].elapsed_time(ev[4]), ev[4].elapsed_time(ev[5]), ev[5].elapsed_time(ev[6]),
@@ -316,15 +317,11 @@ def main():
 
     ms = float(np.mean(step_ms))
     jms = float(np.mean(join_ms))
-    if world > 1:
-        t = torch.tensor([ms, jms, float(pairs)], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        allreduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        allreduce(tsum)
-        ms, jms, total_pairs = float(tmax[0]), float(tmax[1]), int(tsum[2])
-    else:
-        total_pairs = pairs
+    # max over ranks of the device times; pairs summed over ranks
+    t = torch.tensor([ms, jms], dtype=torch.float64, device=dev)
+    comm.all_reduce(t, "max")
+    ms, jms = float(t[0]), float(t[1])
+    total_pairs = int(comm.all_reduce(torch.tensor([pairs], dtype=torch.int64, device=dev))[0])
     value = total_pairs / (ms / 1000.0)
 
     # ---- e2e through the C ABI with host buffers
@@ -341,7 +338,7 @@ def main():
         e2e_s = []
         n_e2e_warm = max(3, args.warmup)   # first host builds grow the library's memory pool
         for i in range(n_e2e_warm + max(7, args.steps)):   # median of >= 7: robust to host-side outliers
-            barrier()
+            comm.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             ixh = Index(host_pts.numpy(), w["eps"], w["k"], stream=stream.cuda_stream, **flags)
@@ -357,10 +354,7 @@ def main():
                 e2e_s.append(dt)
         e2e_t = float(np.median(e2e_s))   # host-side outliers (page faults, pool growth) are rare but large
         e2e_mean = float(np.mean(e2e_s))
-        if world > 1:
-            t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-            allreduce(t, op=dist.ReduceOp.MAX)
-            e2e_t = float(t[0])
+        e2e_t = float(comm.all_reduce(torch.tensor([e2e_t], dtype=torch.float64, device=dev), "max")[0])
         e2e = {"value": total_pairs / e2e_t, "unit": "pairs/s", "seconds": e2e_t, "stat": "median",
                "mean_seconds": e2e_mean, "steps": len(e2e_s),
                "h2d_bytes_per_step": int(N * n * 8), "d2h_bytes_per_step": int(pairs * 8 + 8 * 3 * 8),
@@ -377,17 +371,12 @@ def main():
     filt = info.filter
     roof = None
     if stats is not None:
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tfile):
-            tj = json.load(open(tfile)).get(args.workload, {})
-            traffic = tj.get(f"filter{filt}")
         scale = world if world > 1 else 1
         if filt in (2, 3):
             # certified tensor-core bound: one n-dim dot product (2n flops) per
             # evaluated (unordered) candidate pair, on fp16 operands
             alg = 2.0 * n * stats["tests_evaluated"]
-            # sustained figure: the join kernels run inside a ~200 ms step under the power cap
+            # sustained figure: the join kernels run inside a ~100-200 ms step under the power cap
             peak = peaks.get("bf16_tflops_sustained", 1400.0)
             bound = "tensor"
             kern = ("k_join_umma (tcgen05/TMEM fp16 bound + FP64 decision)" if filt == 2
@@ -404,13 +393,37 @@ def main():
             kern = "k_join32 (FP32 SHORTC prefilter + FP64 decision)" if filt == 1 else "k_join (FP64 SHORTC)"
             pnote = f"derived {'FP32' if filt == 1 else 'FP64'}: {lanes} FMA lanes x 2 flop x {N_SMS} SMs x max clock"
         achieved = alg * scale / (jms / 1000.0) / 1e12
+        # DRAM traffic per join and pipe utilisations: one ncu capture of every
+        # join launch of a step of this workload (tools/ncu_join_traffic.py)
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        tj = traffic_record(args.workload, filt)
+        traffic = tj.get("dram_bytes_per_join") if tj else None
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kern, "peak_note": pnote,
                 "alg": {"tests_evaluated": stats["tests_evaluated"], "dims_evaluated": stats.get("dims_evaluated"),
                         "paper_tests": stats["tests"], "paper_dims": stats.get("dims"), "cells": stats["cells"],
                         "alg_tflop_per_join": alg * scale / 1e12},
                 "join_ms": jms, "join_share_of_step": jms / ms,
-                "filter_margin": info.filter_margin}
+                "filter_margin": info.filter_margin,
+                # HBM view (the north_star's metric): measured DRAM bytes of one join over the
+                # bench's join time, against the measured copy bandwidth
+                "hbm": {"traffic_bytes_per_join": traffic,
+                        "achieved_gbs": traffic / (jms / 1000.0) / 1e9 if traffic else None,
+                        "peak_gbs": hbm_peak,
+                        "frac": traffic / (jms / 1000.0) / 1e9 / hbm_peak if traffic else None,
+                        "peak_note": "measured copy bandwidth, MEASURED_PEAKS.json" if "hbm_gbs" in peaks
+                                     else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                        "note": "the tcgen05 bound makes the join tensor/TMEM-bound; HBM is not its roofline"},
+                "ncu": ({k: tj.get(k) for k in ("tensor_pipe_pct", "fp64_pipe_pct", "fp64_inst_pct", "alu_pipe_pct",
+                                                "issue_pct", "l2_hit_pct", "dram_pct", "launches", "source")}
+                        if tj else None)}
+        if mma_tests is not None and mma_tests > 0:
+            # executed accumulator entries (128 x 128 blocks incl. padding) per evaluated test,
+            # and the executed MMA depth K over the useful n: executed / useful tensor work
+            roof["mma_waste"] = {"mma_tests": mma_tests, "tests_evaluated": stats["tests_evaluated"],
+                                 "block_ratio": mma_tests / max(1, stats["tests_evaluated"]),
+                                 "k_executed": info_k16, "k_useful": n,
+                                 "flop_ratio": mma_tests * 2.0 * info_k16 / max(1.0, alg)}
     line = {
         "metric": "self-join result pairs/s", "value": value, "unit": "pairs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

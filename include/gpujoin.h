@@ -57,7 +57,13 @@ typedef struct {
     int32_t sortidu;     /* 1: SORTIDU prune on the un-indexed dim u (§4.3)               */
     int32_t shortc;      /* 1: SHORTC short-circuit of the distance sum (§4.4)            */
     int32_t symmetric;   /* 1: evaluate each unordered pair once, emit both orders (default);
-                            0: one full neighbour search per query (Alg. 1 verbatim)        */
+                            0: one full neighbour search per query (Alg. 1 verbatim).
+                            With 1, the output of ONE batch or ONE rank is not the
+                            neighbour sets of that share's queries: a pair (a, b) is found
+                            by the share owning the tile of a or of b (whichever comes
+                            first in the symmetric order) and both orders are emitted
+                            there.  Only the union over all batches and ranks is the
+                            self-join.  Use 0 when each share must be query-complete.   */
     double sample_frac;  /* variance sample fraction (§4.2 "1% of |D|"), in (0,1]        */
     uint64_t stream;     /* cudaStream_t the index issues its work on                     */
     int32_t filter;      /* candidate filter of the join kernel; every pair it cannot reject is
@@ -95,7 +101,8 @@ typedef struct {
     float filter_threshold;  /* its rejection threshold (filter 2: in scaled units)      */
     double filter_margin; /* threshold / eps^2 - 1 (relative slack of the bound)          */
     int32_t tile_queries; /* queries per tile: 128, or 256 (filter 2 with mma_tiles = 2)  */
-    int32_t reserved;
+    int32_t mma_depth;    /* filters 2/3: MMA depth K (n + 4 augmented columns rounded up to
+                             16), 0 when the tensor-core operands were not built       */
 } gj_info;
 
 /* Work counters of one join (gj_join_stats).  cells/tests/dims/pairs are the
@@ -214,7 +221,8 @@ GJ_API int gj_self_join(gj_index* idx, uint32_t* out_pairs, int64_t capacity, in
  * result buffers, device->host drains of each batch overlapping the next
  * batch's kernel, into the HOST buffer out_pairs (capacity pairs).  If
  * out_pairs is pinned the drains land in it directly, otherwise through 3
- * pinned staging buffers.  batch_size <= 0 selects b_s = 1e8 (§3.2.2).
+ * pinned staging buffers.  batch_size <= 0 selects the HBM-sized b_s of
+ * gj_num_batches (reading R15), never below the paper's 1e8 (§3.2.2 l.199).
  * On GJ_ERR_CAPACITY *n_pairs holds the required capacity. */
 GJ_API int gj_self_join_host(gj_index* idx, uint32_t* out_pairs, int64_t capacity, int32_t rank,
                       int32_t world, int64_t batch_size, int64_t* n_pairs, int32_t* n_batches_out);
@@ -227,15 +235,28 @@ GJ_API int gj_self_join_host(gj_index* idx, uint32_t* out_pairs, int64_t capacit
  * tensor-core filters, whose unit of work is the evaluated test. */
 GJ_API int gj_join_counts(gj_index* idx, int32_t rank, int32_t world, gj_stats* st);
 
+/* Executed tensor-core work of rank's share (filter 2): the number of
+ * accumulator entries (query row x candidate column of every 128 x 128 MMA
+ * block, padding rows and columns included) the tcgen05 join computes --
+ * divided by gj_stats.tests_evaluated it is the MMA waste ratio.  Runs the
+ * join once in count-only mode (no pairs written).  *mma_tests = -1 when the
+ * index does not run filter 2.  Synchronous. */
+GJ_API int gj_join_mma_tests(gj_index* idx, int32_t rank, int32_t world, int64_t* mma_tests);
+
 /* Work counters of rank's share (cells visited, SORTIDU-window tests,
  * algorithmic SHORTC dims, pairs).  Synchronous; slower than the join. */
 GJ_API int gj_join_stats(gj_index* idx, int32_t rank, int32_t world, gj_stats* st);
 
 /* constructNeighborTable (Alg. 1 l.587): sort n_pairs device pairs by
  * (query, neighbour) in place and write the CSR offsets (n_points + 1
- * uint64, device) of each query's neighbour run.  Synchronous. */
+ * uint64, device) of each query's neighbour run.  Synchronous.
+ * n_pairs must be < 2^32 (32-bit radix-sort offsets): GJ_ERR_INVALID otherwise;
+ * sort larger results per batch. */
 GJ_API int gj_neighbor_table(gj_index* idx, uint32_t* pairs, int64_t n_pairs, uint64_t* offsets);
 
+/* Frees the index.  Synchronises the whole current device first, so joins still
+ * running on caller streams (gj_self_join_async_stream) finish before the
+ * index arrays return to the library pool. */
 GJ_API void gj_free_index(gj_index* idx);
 GJ_API const char* gj_last_error(void);
 GJ_API int32_t gj_abi_version(void);

@@ -263,7 +263,7 @@ int gj_index_info(const gj_index* h, gj_info* info) {
     info->filter_threshold = ix.filter >= 2 ? (float)ix.thr16 : ix.thr32;
     info->filter_margin = ix.filter >= 2 ? ix.margin16 : ix.filter_margin;
     info->tile_queries = ix.tile_q;
-    info->reserved = 0;
+    info->mma_depth = ix.pts16 ? ix.k16 : 0;
     return GJ_OK;
 }
 
@@ -466,10 +466,21 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
         cudaStreamSynchronize(ix.stream);
         if (hcnt) cudaFreeHost(hcnt);
     };
+    // a CUDA error anywhere below records the message and rc, and falls through
+    // to cleanup() (no early return leaks the slot buffers)
+    auto cu = [&](cudaError_t e, const char* what) -> bool {
+        if (e == cudaSuccess) return true;
+        set_error(std::string("gj_self_join_host: ") + what + ": " + cudaGetErrorString(e));
+        if (rc == GJ_OK) rc = GJ_ERR_CUDA;
+        return false;
+    };
     for (int i = 0; i < 3; ++i) {
         if (!ix.pipe_stream[i]) {
-            GJ_CUDA(cudaStreamCreateWithFlags(&ix.pipe_stream[i], cudaStreamNonBlocking));
-            GJ_CUDA(cudaEventCreateWithFlags(&ix.pipe_event[i], cudaEventDisableTiming));
+            if (!cu(cudaStreamCreateWithFlags(&ix.pipe_stream[i], cudaStreamNonBlocking), "stream") ||
+                !cu(cudaEventCreateWithFlags(&ix.pipe_event[i], cudaEventDisableTiming), "event")) {
+                cleanup();
+                return rc;
+            }
         }
         if (pool_malloc(&dbuf[i], (size_t)per * 2 * sizeof(uint32_t), ix.stream) != cudaSuccess ||
             (!direct && cudaMallocHost(&hbuf[i], (size_t)per * 2 * sizeof(uint32_t)) != cudaSuccess)) {
@@ -486,17 +497,16 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
         return GJ_ERR_NOMEM;
     }
     // the pipeline streams wait for the index build on the index stream
-    cudaEvent_t ready;
-    GJ_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    GJ_CUDA(cudaEventRecord(ready, ix.stream));
-    for (int i = 0; i < 3; ++i) GJ_CUDA(cudaStreamWaitEvent(ix.pipe_stream[i], ready, 0));
-    cudaEventDestroy(ready);
+    cudaEvent_t ready = nullptr;
+    if (cu(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event") && cu(cudaEventRecord(ready, ix.stream), "record"))
+        for (int i = 0; i < 3 && rc == GJ_OK; ++i) cu(cudaStreamWaitEvent(ix.pipe_stream[i], ready, 0), "wait");
+    if (ready) cudaEventDestroy(ready);
 
     int64_t pending_n[3] = {0, 0, 0};
     int64_t pending_at[3] = {-1, -1, -1};
     auto drain = [&](int i) -> int {   // host side of batch in slot i ("Table" stage)
         if (pending_at[i] < 0) return GJ_OK;
-        GJ_CUDA(cudaEventSynchronize(ix.pipe_event[i]));
+        if (!cu(cudaEventSynchronize(ix.pipe_event[i]), "drain")) return rc;
         if (!direct && pending_n[i] > 0 && pending_at[i] + pending_n[i] <= capacity)
             memcpy(out_pairs + 2 * pending_at[i], hbuf[i], (size_t)pending_n[i] * 2 * sizeof(uint32_t));
         pending_at[i] = -1;
@@ -505,18 +515,19 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
     for (int64_t b = 0; b < nb && rc == GJ_OK; ++b) {
         const int i = (int)(b % 3);
         cudaStream_t st = ix.pipe_stream[i];
-        if ((rc = drain(i))) break;
+        if (drain(i) != GJ_OK) break;
         // kernel (retry with a larger buffer if the estimate was low)
         for (;;) {
-            GJ_CUDA(cudaMemsetAsync(dcnt + i, 0, sizeof(uint64_t), st));
+            if (!cu(cudaMemsetAsync(dcnt + i, 0, sizeof(uint64_t), st), "memset")) break;
             JoinArgs a{};
             a.out = dbuf[i];
             a.cap = (uint64_t)cap_of[i];
             a.count = dcnt + i;
             batch_tiles(&ix, (int32_t)b, (int32_t)nb, rank, world, &a);
             if ((rc = launch_join(&ix, kEmit, a, st))) break;
-            GJ_CUDA(cudaMemcpyAsync(hcnt + i, dcnt + i, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-            GJ_CUDA(cudaStreamSynchronize(st));
+            if (!cu(cudaMemcpyAsync(hcnt + i, dcnt + i, sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "count D2H") ||
+                !cu(cudaStreamSynchronize(st), "batch"))
+                break;
             if ((int64_t)hcnt[i] <= cap_of[i]) break;
             // re-plan: grow this slot's buffers and rerun the batch (§3.2.2 estimate was low)
             cap_of[i] = (int64_t)hcnt[i] + 1024;
@@ -534,15 +545,15 @@ int gj_self_join_host(gj_index* h, uint32_t* out_pairs, int64_t capacity, int32_
         if (written + cnt > capacity) overflow = true;
         if (cnt > 0 && !overflow) {
             void* dst = direct ? (void*)(out_pairs + 2 * written) : (void*)hbuf[i];
-            GJ_CUDA(cudaMemcpyAsync(dst, dbuf[i], (size_t)cnt * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            if (!cu(cudaMemcpyAsync(dst, dbuf[i], (size_t)cnt * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "pairs D2H")) break;
         }
-        GJ_CUDA(cudaEventRecord(ix.pipe_event[i], st));
+        if (!cu(cudaEventRecord(ix.pipe_event[i], st), "record")) break;
         pending_at[i] = overflow ? -2 : written;
         pending_n[i] = cnt;
         if (overflow) pending_at[i] = -1;
         written += cnt;
     }
-    for (int i = 0; i < 3 && rc == GJ_OK; ++i) rc = drain(i);
+    for (int i = 0; i < 3 && rc == GJ_OK; ++i) drain(i);
     for (int i = 0; i < 3; ++i) cudaStreamSynchronize(ix.pipe_stream[i]);
     cleanup();
     *n_pairs = written;
@@ -572,6 +583,25 @@ int gj_join_counts(gj_index* h, int32_t rank, int32_t world, gj_stats* st) {
     return GJ_OK;
 }
 
+int gj_join_mma_tests(gj_index* h, int32_t rank, int32_t world, int64_t* mma_tests) {
+    if (!h || !mma_tests) { set_error("null argument"); return GJ_ERR_INVALID; }
+    if (int rc = check_rank(rank, world)) return rc;
+    Index& ix = h->ix;
+    *mma_tests = -1;
+    if (ix.filter != 2) return GJ_OK;
+    JoinArgs a{};
+    a.count = ix.scratch_count;
+    a.mma_tests = (unsigned long long*)ix.scratch_count + 4;
+    batch_tiles(&ix, 0, 1, rank, world, &a);
+    GJ_CUDA(cudaMemsetAsync(ix.scratch_count, 0, 8 * sizeof(uint64_t), ix.stream));
+    if (int rc = launch_join(&ix, kCount, a, ix.stream)) return rc;
+    uint64_t c = 0;
+    GJ_CUDA(cudaMemcpyAsync(&c, ix.scratch_count + 4, sizeof(c), cudaMemcpyDeviceToHost, ix.stream));
+    GJ_CUDA(cudaStreamSynchronize(ix.stream));
+    *mma_tests = (int64_t)c;
+    return GJ_OK;
+}
+
 int gj_join_stats(gj_index* h, int32_t rank, int32_t world, gj_stats* st) {
     if (!h || !st) { set_error("null argument"); return GJ_ERR_INVALID; }
     if (int rc = check_rank(rank, world)) return rc;
@@ -595,6 +625,8 @@ int gj_join_stats(gj_index* h, int32_t rank, int32_t world, gj_stats* st) {
 
 int gj_neighbor_table(gj_index* h, uint32_t* pairs, int64_t n_pairs, uint64_t* offsets) {
     if (!h || (n_pairs > 0 && !pairs) || !offsets || n_pairs < 0) { set_error("bad argument"); return GJ_ERR_INVALID; }
+    // the radix sort's histogram scan and scatter offsets are 32-bit
+    if (n_pairs > (int64_t)UINT32_MAX) { set_error("gj_neighbor_table: n_pairs > 2^32-1"); return GJ_ERR_INVALID; }
     Index& ix = h->ix;
     cudaStream_t s = ix.stream;
     uint64_t* keys = nullptr;
@@ -622,6 +654,11 @@ int gj_neighbor_table(gj_index* h, uint32_t* pairs, int64_t n_pairs, uint64_t* o
 void gj_free_index(gj_index* h) {
     if (!h) return;
     Index& ix = h->ix;
+    // joins launched with gj_self_join_async_stream on caller streams may still
+    // read pts / pts16 / nbr: wait for all work on the device before the arrays
+    // go back to the pool (which reuses them at once)
+    cudaDeviceSynchronize();
+    cudaGetLastError();
     void* ptrs[] = {ix.pts, ix.pts32, ix.pts16, ix.norm16, ix.orig, ix.cell_id, ix.cell_start, ix.nbr_off, ix.nbr, ix.nbr_self, ix.tile_cell, ix.tile_q0,
                     ix.tile_order, ix.tile_work, ix.meta, ix.scratch_count};
     for (void* p : ptrs)   // back to the library pool (stream-ordered)

@@ -129,6 +129,9 @@ struct JoinArgs {
     // part_off[m+1] - part_off[m] CTAs; part_off[n_tiles] = total parts.
     const uint32_t* part_off;
     int64_t total_parts;
+    // optional (tcgen05 join): += MMA tests executed (rows x columns of every
+    // accumulator block, padding included) -- the executed-vs-useful ratio
+    unsigned long long* mma_tests;
 };
 struct JoinParams {
     const double* __restrict__ pts;

@@ -20,7 +20,7 @@ GJ_OK, GJ_ERR_INVALID, GJ_ERR_CUDA, GJ_ERR_OVERFLOW, GJ_ERR_CAPACITY, GJ_ERR_NOM
 # Every symbol include/gpujoin.h declares (checked by tests/test_capi_cpu.py).
 EXPORTS = ["gj_default_options", "gj_build_index", "gj_index_info", "gj_dim_order", "gj_device_arrays",
            "gj_estimate", "gj_num_batches", "gj_partition", "gj_fp32_threshold", "gj_fp32_accept_threshold", "gj_tc_threshold", "gj_selftest_umma", "gj_self_join_async", "gj_self_join_async_stream", "gj_self_join_count_async", "gj_self_join",
-           "gj_self_join_host", "gj_join_stats", "gj_join_counts", "gj_neighbor_table", "gj_free_index", "gj_last_error",
+           "gj_self_join_host", "gj_join_stats", "gj_join_counts", "gj_join_mma_tests", "gj_neighbor_table", "gj_free_index", "gj_last_error",
            "gj_abi_version", "gj_launch_count", "gj_release_cached_memory"]
 
 
@@ -35,7 +35,7 @@ class Info(C.Structure):
                 ("u", C.c_int32), ("eps", C.c_double), ("n_cells", C.c_int64), ("n_adjacent", C.c_int64),
                 ("n_tiles", C.c_int64), ("est_candidates", C.c_double), ("build_ms", C.c_double),
                 ("filter", C.c_int32), ("filter_threshold", C.c_float), ("filter_margin", C.c_double),
-                ("tile_queries", C.c_int32), ("reserved", C.c_int32)]
+                ("tile_queries", C.c_int32), ("mma_depth", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -81,6 +81,7 @@ def lib():
         "gj_self_join_host": (C.c_int, [P, P, I64, I32, I32, I64, C.POINTER(I64), C.POINTER(C.c_int32)]),
         "gj_join_stats": (C.c_int, [P, I32, I32, C.POINTER(Stats)]),
         "gj_join_counts": (C.c_int, [P, I32, I32, C.POINTER(Stats)]),
+        "gj_join_mma_tests": (C.c_int, [P, I32, I32, C.POINTER(I64)]),
         "gj_neighbor_table": (C.c_int, [P, P, I64, P]),
         "gj_free_index": (None, [P]),
         "gj_last_error": (C.c_char_p, []),
@@ -228,6 +229,12 @@ class Index:
         s = Stats()
         _check(lib().gj_join_counts(self._h, rank, world, C.byref(s)))
         return dict(cells=s.cells, tests=s.tests, tests_evaluated=s.tests_evaluated)
+
+    def mma_tests(self, rank=0, world=1) -> int:
+        """Executed tensor-core accumulator entries of the share (gj_join_mma_tests; -1 if not filter 2)."""
+        v = C.c_int64(0)
+        _check(lib().gj_join_mma_tests(self._h, rank, world, C.byref(v)))
+        return int(v.value)
 
     def neighbor_table(self, pairs, n_pairs, offsets):
         _check(lib().gj_neighbor_table(self._h, _ptr(pairs), int(n_pairs), _ptr(offsets)))

@@ -26,12 +26,16 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1809_09930_b200 import distributed as D
+        comm = D.Comm()
+        assert (comm.rank, comm.world, comm.backend) == (rank, world, "gloo")
         pts = torch.arange(24, dtype=torch.float64).reshape(6, 4) if rank == 0 else torch.zeros(6, 4, dtype=torch.float64)
-        D.replicate(pts)
+        comm.broadcast(pts)
         cnt = torch.tensor([10 * (rank + 1)], dtype=torch.int64)
-        tot = D.global_count(cnt.clone())
+        tot = comm.all_reduce(cnt.clone())
+        mx = comm.all_reduce(torch.tensor([1.5 * (rank + 1)], dtype=torch.float64), "max")
+        comm.barrier()
         mine = D.share_positions(37, rank, world, 0, 1).tolist()
-        q.put((rank, pts.sum().item(), int(tot.item()), mine))
+        q.put((rank, pts.sum().item(), int(tot.item()), mine, float(mx.item())))
     finally:
         dist.destroy_process_group()
 
@@ -55,6 +59,7 @@ def test_two_rank_gloo_replicate_allreduce_partition():
         assert p.exitcode == 0
     assert all(r[1] == float(sum(range(24))) for r in res)          # every rank holds D
     assert all(r[2] == 30 for r in res)                              # 10 + 20
+    assert all(r[4] == 3.0 for r in res)                             # max over ranks (bench timing)
     allpos = sorted(res[0][3] + res[1][3])
     assert allpos == list(range(37))                                 # disjoint, complete
     assert res[0][3] == list(range(0, 37, 2))

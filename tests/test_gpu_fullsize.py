@@ -40,16 +40,20 @@ def bench_launch(ix, rank=0, world=1, b_s=0):
 
 
 def sampled_check(D, eps, pairs, qids):
+    """Complete neighbour list of every sampled query == the oracle's (the
+    ambiguous band counted and recorded for the parity report)."""
+    from conftest import record_band
     q_t = torch.from_numpy(qids).to("cuda", torch.int32)
     sel = pairs[torch.isin(pairs[:, 0], q_t)].cpu().numpy().astype(np.int64)
-    amb_total = 0
+    n_sure = n_amb = n_amb_in = 0
     for qi, (sure, amb) in zip(qids, brute.neighbors_of(D, eps, qids)):
         got = np.sort(sel[sel[:, 0] == qi, 1])
         assert len(np.unique(got)) == len(got), "duplicate neighbour"
         S, G, A = set(sure.tolist()), set(got.tolist()), set(amb.tolist())
         assert S <= G and G <= S | A, (qi, len(S - G), len(G - S - A))
-        amb_total += len(A)
-    return amb_total
+        n_sure, n_amb, n_amb_in = n_sure + len(S), n_amb + len(A), n_amb_in + len(G & A)
+    record_band(n_sure, n_amb, n_amb_in)
+    return n_amb
 
 
 def global_properties(pairs, N):
@@ -64,12 +68,45 @@ def global_properties(pairs, N):
     assert selfs.numel() == N and torch.unique(selfs).numel() == N, "self pairs missing"
 
 
-@pytest.mark.parametrize("workload,nq", [("expo32", 40), ("uniform16", 24), ("songs90", 24)])
-def test_full_size_sampled_and_global(workload, nq):
+# Every config point bench.py or DESIGN.md reports (BASELINE.json configs[1..3],
+# PAPER.md l.876-877 k sweep, l.968-970 eps ranges), with the flags it runs:
+# (workload, eps override, k override, Index flags, sampled queries).
+POINTS = [
+    ("uniform16", 0.50, None, {}, 24),
+    ("uniform16", 0.55, None, {}, 24),
+    ("uniform16", 0.60, None, {}, 24),
+    ("expo16", None, None, {}, 24),
+    ("expo32", None, None, {}, 40),
+    ("expo32", None, None, {"reorder": False}, 24),
+    ("expo32", None, None, {"sortidu": False}, 24),
+    ("songs90", 0.005, 4, {}, 24),
+    ("songs90", 0.005, 5, {}, 24),
+    ("songs90", 0.005, 6, {}, 24),
+    ("songs90", 0.005, 7, {}, 24),
+    ("songs90", 0.005, 8, {}, 24),
+    ("songs90", 0.01, 6, {}, 16),
+]
+_DATA = {}
+
+
+def _data(workload):
+    if workload not in _DATA:
+        _DATA.clear()
+        w = synth.WORKLOADS[workload]
+        _DATA[workload] = synth.make(w["gen"], w["count"], w["dims"], seed=0)
+    return _DATA[workload]
+
+
+@pytest.mark.parametrize("workload,eps,k,flags,nq", POINTS,
+                         ids=[f"{w}-eps{e}-k{k}-{'-'.join(f'{a}{int(b)}' for a, b in f.items()) or 'default'}"
+                              for w, e, k, f, _ in POINTS])
+def test_full_size_sampled_and_global(workload, eps, k, flags, nq):
     from paper_1809_09930_b200 import Index
     w = synth.WORKLOADS[workload]
-    D = synth.make(w["gen"], w["count"], w["dims"], seed=0)
-    ix = Index(torch.from_numpy(D).cuda(), w["eps"], w["k"])
+    eps = w["eps"] if eps is None else eps
+    k = w["k"] if k is None else k
+    D = _data(workload)
+    ix = Index(torch.from_numpy(D).cuda(), eps, k, **flags)
     pairs, nb = bench_launch(ix)
     assert nb >= 3
     global_properties(pairs, len(D))
@@ -78,21 +115,27 @@ def test_full_size_sampled_and_global(workload, nq):
     torch.cuda.synchronize()
     assert int(cnt[0].item()) == pairs.shape[0]
     qids = synth.query_sample(len(D), nq, seed=11)
-    sampled_check(D, w["eps"], pairs, qids)
+    sampled_check(D, eps, pairs, qids)
     assert pairs.shape[0] > len(D)
+    del pairs, ix
+    torch.cuda.empty_cache()
 
 
-def test_expo64_10m_entity_partition_share():
-    """configs[4] at full size: one rank's share of a 2000-way entity
-    partition (per-query mode, so every query of the share has its complete
-    neighbour list) against the oracle."""
+@pytest.mark.parametrize("rank", [7, 1000, 1999])
+def test_expo64_10m_entity_partition_share(rank):
+    """configs[4] at full size: rank shares of a 2000-way entity partition
+    (per-query mode, so every query of the share has its complete neighbour
+    list) against the oracle; the heaviest (rank 7: early in the
+    heaviest-first order), a middle and the last share."""
     from paper_1809_09930_b200 import Index
     w = synth.WORKLOADS["expo64_10m"]
-    D = synth.make(w["gen"], w["count"], w["dims"], seed=0)
+    D = _data("expo64_10m")
     ix = Index(torch.from_numpy(D).cuda(), w["eps"], w["k"], symmetric=False)
-    world, rank = 2000, 7
+    world = 2000
     pairs, _ = bench_launch(ix, rank, world)
     qs = torch.unique(pairs[:, 0]).cpu().numpy().astype(np.int64)
     assert len(qs) > 100
-    qids = np.sort(np.random.default_rng(5).choice(qs, 12, replace=False))
+    qids = np.sort(np.random.default_rng(5 + rank).choice(qs, 12, replace=False))
     sampled_check(D, w["eps"], pairs, qids)
+    del pairs, ix
+    torch.cuda.empty_cache()

@@ -37,6 +37,10 @@ def gpu_pairs(D, eps, k, world=1, rank=None, **flags):
 
 
 def check(D, eps, got):
+    """Exact pair-set parity with the brute-force oracle.  Returns
+    (ambiguous-band pairs, how many of them the GPU emitted); the counts are
+    also recorded for the parity report (conftest.parity_report)."""
+    from conftest import record_band
     sure, amb = brute.self_join(D, eps)
     S = {tuple(r) for r in sure.tolist()}
     A = {tuple(r) for r in amb.tolist()}
@@ -44,6 +48,7 @@ def check(D, eps, got):
     assert len(G) == len(got), "duplicate pairs emitted"
     missing, extra = S - G, G - S - A
     assert not missing and not extra, (len(missing), len(extra), list(missing)[:5], list(extra)[:5])
+    record_band(len(S), len(A), len(G & A))
     return len(A), len(G & A)
 
 
@@ -259,37 +264,53 @@ def test_join_counts_equal_stats_scan(sortidu, symmetric, mma_tiles):
 
 
 @pytest.mark.parametrize("symmetric", [0, 1])
-def test_entity_partition_union_equals_single_gpu(symmetric):
+def test_entity_partition_union_equals_oracle(symmetric):
+    """§6.2: the shares of 4 ranks are disjoint and their union is the oracle's
+    self-join; with symmetric = 0 every share is query-complete (it holds
+    exactly the oracle's pairs of the queries it owns)."""
     D = synth.exponential(4000, 16, seed=21)
-    full, _ = gpu_pairs(D, 0.045, 6, symmetric=symmetric)
     parts = [gpu_pairs(D, 0.045, 6, world=4, rank=r, symmetric=symmetric)[0] for r in range(4)]
-    F = {tuple(r) for r in full.tolist()}
     U = [{tuple(r) for r in p.tolist()} for p in parts]
-    assert sum(len(u) for u in U) == len(F)
-    assert set().union(*U) == F
+    assert sum(len(u) for u in U) == len(set().union(*U))      # disjoint shares
+    check(D, 0.045, np.concatenate(parts))
+    if not symmetric:
+        owners = [{a for a, _ in u} for u in U]
+        assert sum(len(o) for o in owners) == len(D)             # every query owned by one rank
+        sure, amb = brute.self_join(D, 0.045)
+        assert len(amb) == 0
+        for u, o in zip(U, owners):
+            assert u == {tuple(r) for r in sure.tolist() if r[0] in o}
 
 
-def test_batches_and_host_pipeline_equal_single_launch():
+def _np_pairs(t):
+    return t.cpu().numpy().view(np.uint32).astype(np.int64)
+
+
+def test_batches_and_host_pipeline_equal_oracle():
+    """Batched device launches (§3.2.2) and the Fig. 4 host pipeline
+    (gj_self_join_host, the call the bench's e2e number runs through), into
+    pageable and pinned host memory: each pair set equals the oracle's."""
     from paper_1809_09930_b200 import Index
     D = synth.exponential(5000, 16, seed=4)
     ix = Index(torch.from_numpy(D).cuda(), 0.045, 6)
     cap = ix.estimate(1.0) + 4096
     out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
     n = ix.self_join(out)
-    ref = {tuple(r) for r in out[:n].cpu().numpy().tolist()}
+    check(D, 0.045, _np_pairs(out[:n]))
     # 5 batches into one device buffer
+    out.fill_(-1)
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     for b in range(5):
         ix.self_join_async(out, cnt, b, 5)
     torch.cuda.synchronize()
     assert int(cnt.item()) == n
-    assert {tuple(r) for r in out[:n].cpu().numpy().tolist()} == ref
+    check(D, 0.045, _np_pairs(out[:n]))
     # Fig. 4 pipeline into pageable and pinned host buffers, small b_s -> many batches
     for pinned in (False, True):
-        host = torch.empty((cap, 2), dtype=torch.int32, pin_memory=pinned)
+        host = torch.full((cap, 2), -1, dtype=torch.int32, pin_memory=pinned)
         m, nb = ix.self_join_host(host, batch_size=max(1, n // 7))
         assert m == n and nb >= 7
-        assert {tuple(r) for r in host[:m].numpy().tolist()} == ref
+        check(D, 0.045, _np_pairs(host[:m]))
     # capacity error reports the needed size
     from paper_1809_09930_b200 import GpuJoinError
     with pytest.raises(GpuJoinError):
@@ -304,28 +325,30 @@ from paper_1809_09930_b200 import Index
 D = synth.exponential(6000, 16, seed=9)
 ix = Index(torch.from_numpy(D).cuda(), 0.045, 6)
 cap = ix.estimate(1.0) + 4096
-out = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
-n = ix.self_join(out)
-ref = sorted(map(tuple, out[:n].cpu().numpy().tolist()))
 for pinned in (False, True):
-    host = torch.empty((cap, 2), dtype=torch.int32, pin_memory=pinned)
-    m, nb = ix.self_join_host(host, batch_size=max(1, n // 5))
-    assert m == n and nb >= 5, (m, n, nb)
-    assert sorted(map(tuple, host[:m].numpy().tolist())) == ref
-print("regrow ok", n, nb)
+    host = torch.full((cap, 2), -1, dtype=torch.int32, pin_memory=pinned)
+    m, nb = ix.self_join_host(host, batch_size=max(1, cap // 5))
+    assert nb >= 5, (m, nb)
+    np.save(sys.argv[2] + ("_pinned" if pinned else "_pageable") + ".npy", host[:m].numpy())
+print("regrow ok", m, nb)
 """
 
 
-def test_host_pipeline_regrows_underestimated_batches():
+def test_host_pipeline_regrows_underestimated_batches(tmp_path):
     """GJ_BATCH_HEADROOM=0.05 makes every result slot far too small for its
-    batch: each slot is regrown on its own and the batch rerun (§3.2.2), the
-    pairs identical to one device launch."""
+    batch: each slot is regrown on its own and the batch rerun (§3.2.2); the
+    pairs (pageable and pinned host output) equal the oracle's."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, GJ_BATCH_HEADROOM="0.05")
-    r = subprocess.run([sys.executable, "-c", _REGROW_SCRIPT, root], env=env, capture_output=True, text=True,
+    stem = str(tmp_path / "pairs")
+    r = subprocess.run([sys.executable, "-c", _REGROW_SCRIPT, root, stem], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "regrow ok" in r.stdout, r.stdout + r.stderr
+    D = synth.exponential(6000, 16, seed=9)
+    for kind in ("pageable", "pinned"):
+        got = np.load(f"{stem}_{kind}.npy").view(np.uint32).astype(np.int64)
+        check(D, 0.045, got)
 
 
 def test_neighbor_table():

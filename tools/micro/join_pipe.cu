@@ -15,9 +15,29 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "gj_umma.cuh"
 using namespace gj;
+
+// VAR bit 0: no candidate loads (the producer arrives on `full` without a copy);
+// bit 1: no accumulator reads (the epilogue releases the slot at once).
+// bit 2: mbarrier waits without the suspend-time hint (plain try_wait spin).
+// bit 3: stream sequentially through the whole (large) source buffer from a
+//        CTA-specific start instead of cycling over the first 512 blocks.
+// bit 4: random A operand (the B source is filled by the host: zeros, or random
+//        values when main() is given a second argument).
+__device__ __forceinline__ void wait_spin(uint64_t* mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITS_%=;\n\t}\n" ::"r"(umma::smem_u32(mbar)), "r"(parity));
+}
+template <int VAR>
+__device__ __forceinline__ void wait(uint64_t* mbar, uint32_t parity) {
+    if (VAR & 4) wait_spin(mbar, parity); else umma::mbar_wait(mbar, parity);
+}
 
 template <int KP, int BN, int SLOTS, int NEW, int CP, int ST>
 struct Smem {
@@ -28,7 +48,7 @@ struct Smem {
     unsigned hits;
 };
 
-template <int KP, int BN, int SLOTS, int NEW, int CP, int ST, int CTAS>
+template <int KP, int BN, int SLOTS, int NEW, int CP, int ST, int CTAS, int VAR>
 __global__ void __launch_bounds__(64 + 32 * NEW, CTAS)
     k_pipe(const __half* __restrict__ bsrc, int nsrc_blocks, int iters, long long* out, unsigned* hits) {
     extern __shared__ __align__(1024) unsigned char raw[];
@@ -38,11 +58,15 @@ __global__ void __launch_bounds__(64 + 32 * NEW, CTAS)
     constexpr int NL = CW / 32;                 // x32 loads per warp per block
     constexpr uint32_t TCOLS = SLOTS * BN <= 128 ? 128 : (SLOTS * BN <= 256 ? 256 : 512);
     static_assert(SLOTS * BN <= 512, "TMEM");
+    // a warp group must own whole slots, else a group waiting on block c could
+    // see the completion of block c - 2 SLOTS on the same barrier parity
+    static_assert(GROUPS >= 1 && SLOTS % GROUPS == 0, "groups must divide slots");
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 128 * KP; i += blockDim.x) {
         const int row = i / KP, k = i % KP;
+        const float av = (VAR & 16) ? (float)((row * 131 + k * 71) % 97) / 48.5f - 1.f : (k == 0 ? -1.f : 0.f);
         *reinterpret_cast<__half*>(reinterpret_cast<unsigned char*>(S.a) + umma::tile_off(row, k, KP)) =
-            __float2half(k == 0 ? -1.f : 0.f);
+            __float2half(av);
     }
     if (warp == 1) umma::tmem_alloc(&S.tbase, TCOLS);
     if (threadIdx.x == 0) {
@@ -62,9 +86,11 @@ __global__ void __launch_bounds__(64 + 32 * NEW, CTAS)
         if (lane == 0) {
             for (int c = 0; c < iters; ++c) {
                 const uint32_t st = c % ST, ph = (c / ST) & 1u;
-                umma::mbar_wait(&S.empty[st], ph ^ 1u);
+                wait<VAR>(&S.empty[st], ph ^ 1u);
+                if (VAR & 1) { umma::mbar_arrive(&S.full[st]); continue; }
                 umma::mbar_arrive_expect_tx(&S.full[st], kBlockBytes);
-                const int sb = (c + 7 * blockIdx.x) % nsrc_blocks;
+                const int sb = (VAR & 8) ? (int)(((long long)blockIdx.x * 977 + c) % nsrc_blocks)
+                                         : (c + 7 * blockIdx.x) % 512;
                 umma::bulk_g2s(umma::smem_u32(S.b[st]), bsrc + (size_t)sb * BN * KP, kBlockBytes, &S.full[st]);
             }
         }
@@ -73,8 +99,8 @@ __global__ void __launch_bounds__(64 + 32 * NEW, CTAS)
             constexpr uint32_t idesc = umma::idesc_f16_f32(128, BN);
             for (int c = 0; c < iters; ++c) {
                 const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c % SLOTS, aph = (c / SLOTS) & 1u;
-                umma::mbar_wait(&S.acce[ab], aph ^ 1u);
-                umma::mbar_wait(&S.full[st], ph);
+                wait<VAR>(&S.acce[ab], aph ^ 1u);
+                wait<VAR>(&S.full[st], ph);
                 umma::fence_after();
 #pragma unroll
                 for (int ks = 0; ks < KP / 16; ++ks)
@@ -89,8 +115,13 @@ __global__ void __launch_bounds__(64 + 32 * NEW, CTAS)
         unsigned found = 0;
         for (int c = grp; c < iters; c += GROUPS) {
             const uint32_t ab = c % SLOTS, aph = (c / SLOTS) & 1u;
-            umma::mbar_wait(&S.accf[ab], aph);
+            wait<VAR>(&S.accf[ab], aph);
             umma::fence_after();
+            if (VAR & 2) {
+                __syncwarp();
+                if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                continue;
+            }
             const uint32_t tcol = tmem + ((uint32_t)(32 * q) << 16) + ab * BN + cp * CW;
             uint32_t acc = 0xffffffffu;
             constexpr int NC = NL >= 2 ? 2 : 1;
@@ -129,10 +160,11 @@ __global__ void __launch_bounds__(64 + 32 * NEW, CTAS)
     if (warp == 1) umma::tmem_dealloc(tmem, TCOLS);
 }
 
-template <int KP, int BN, int SLOTS, int NEW, int CP, int ST = 4, int CTAS = 1>
-void run(const char* name, const __half* src, int nsrc) {
+template <int KP, int BN, int SLOTS, int NEW, int CP, int ST = 4, int CTAS = 1, int VAR = 0>
+void run(const char* name, const __half* src, int nsrc_unused) {
+    const int nsrc = (int)((size_t)8192 * 256 * 48 / (BN * KP));   // whole buffer in blocks
     using Sm = Smem<KP, BN, SLOTS, NEW, CP, ST>;
-    auto kern = k_pipe<KP, BN, SLOTS, NEW, CP, ST, CTAS>;
+    auto kern = k_pipe<KP, BN, SLOTS, NEW, CP, ST, CTAS, VAR>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Sm));
     long long* d; cudaMalloc(&d, 148 * CTAS * 8);
     unsigned* hits; cudaMalloc(&hits, 4); cudaMemset(hits, 0, 4);
@@ -149,35 +181,40 @@ void run(const char* name, const __half* src, int nsrc) {
     printf("%-48s: %7.1f cyc/blk/CTA  %6.1f tests/clk/SM  %.2f Ttests/s  mma-ideal %4.0f cyc  hits %u %s\n", name,
            (double)c / iters, tests / c, tests * 148 / (ms * 1e-3) / 1e12, (KP / 16) * 128.0 * BN / 256.0, h,
            cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
     cudaFree(d); cudaFree(hits);
 }
 
-int main() {
-    const int nsrc = 512;   // 512 blocks of 256 x 48 fp16 = 12.6 MB, L2 resident
-    __half* src; cudaMalloc(&src, (size_t)nsrc * 256 * 128 * 2);
-    {   // all-zero operands: every accumulator is +0 (the timing does not depend on the values)
-        const size_t tot = (size_t)nsrc * 256 * 128;
+int main(int argc, char** argv) {
+    // 8192 blocks of 256 x 48 fp16 = 201 MB (bit 3 streams through all of it; otherwise
+    // the first 512 blocks, 12.6 MB, L2 resident)
+    const int nsrc = 8192;
+    __half* src; cudaMalloc(&src, (size_t)nsrc * 256 * 48 * 2);
+    {
+        const size_t tot = (size_t)nsrc * 256 * 48;
         __half* h = (__half*)malloc(tot * 2);
-        for (size_t i = 0; i < tot; ++i) h[i] = __float2half(0.f);
+        const bool rnd = argc > 2;
+        unsigned x = 12345;
+        for (size_t i = 0; i < tot; ++i) {
+            x = x * 1664525u + 1013904223u;
+            h[i] = __float2half(rnd ? (float)(x >> 8) / 8388608.f - 1.f : 0.f);
+        }
         cudaMemcpy(src, h, tot * 2, cudaMemcpyHostToDevice);
         free(h);
     }
-    run<48, 128, 1, 4, 1, 2, 4>("K48 N128 4 CTAs x (1 slot, 4 warps) [current]", src, nsrc);
-    run<32, 128, 1, 4, 1, 2, 4>("K32 N128 4 CTAs x (1 slot, 4 warps)", src, nsrc);
-    run<48, 128, 2, 8, 1, 3, 2>("K48 N128 2 CTAs x (2 slots, 2 groups)", src, nsrc);
-    run<48, 128, 2, 8, 2, 3, 2>("K48 N128 2 CTAs x (2 slots, 8 warps 2 col)", src, nsrc);
-    run<48, 128, 4, 16, 4>("K48 N128 4 slots 16 warps (4 col parts)", src, nsrc);
-    run<48, 128, 4, 16, 1>("K48 N128 4 slots 16 warps (4 groups)", src, nsrc);
-    run<48, 128, 4, 16, 2>("K48 N128 4 slots 16 warps (2 col x 2 grp)", src, nsrc);
-    run<48, 128, 4, 8, 2>("K48 N128 4 slots 8 warps (2 col parts)", src, nsrc);
-    run<48, 128, 4, 8, 1>("K48 N128 4 slots 8 warps (2 groups)", src, nsrc);
-    run<48, 256, 2, 16, 4>("K48 N256 2 slots 16 warps (4 col parts)", src, nsrc);
-    run<32, 128, 4, 16, 4>("K32 N128 4 slots 16 warps (4 col parts)", src, nsrc);
-    run<32, 128, 4, 16, 1>("K32 N128 4 slots 16 warps (4 groups)", src, nsrc);
-    run<32, 128, 4, 16, 2>("K32 N128 4 slots 16 warps (2 col x 2 grp)", src, nsrc);
-    run<32, 256, 2, 16, 4>("K32 N256 2 slots 16 warps (4 col parts)", src, nsrc);
-    run<32, 128, 4, 24, 2>("K32 N128 4 slots 24 warps (2 col x 3 grp)", src, nsrc);
-    run<32, 128, 4, 24, 1>("K32 N128 4 slots 24 warps (6 grp)", src, nsrc);
-    run<48, 128, 4, 24, 2>("K48 N128 4 slots 24 warps (2 col x 3 grp)", src, nsrc);
+    const int pick = argc > 1 ? atoi(argv[1]) : -1;
+    int idx = 0;
+    if (pick < 0 || pick == idx) run<48,128,2,8,2,7,2,0>("K48 N128 2x(2 slots, 8w) ST7 zeros, L2 src", src, nsrc);
+    ++idx;
+    if (pick < 0 || pick == idx) run<48,128,2,8,2,7,2,8>("K48 ... streaming 200 MB src", src, nsrc);
+    ++idx;
+    if (pick < 0 || pick == idx) run<48,128,2,8,2,7,2,16>("K48 ... random A", src, nsrc);
+    ++idx;
+    if (pick < 0 || pick == idx) run<48,128,2,8,2,7,2,24>("K48 ... random A + streaming", src, nsrc);
+    ++idx;
+    if (pick < 0 || pick == idx) run<48,128,1,4,1,2,4,0>("K48 current 4x(1 slot) zeros", src, nsrc);
+    ++idx;
+    if (pick < 0 || pick == idx) run<48,128,1,4,1,2,4,24>("K48 current 4x(1 slot) random A + streaming", src, nsrc);
+    ++idx;
     return 0;
 }

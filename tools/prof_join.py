@@ -17,6 +17,7 @@ p.add_argument("--eps", type=float, default=None)
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--filter", type=int, default=2)
 p.add_argument("--mma-tiles", type=int, default=0)
+p.add_argument("--batches", type=int, default=1, help="result batches (bench: 3); batch b = every n_b-th tile")
 a = p.parse_args()
 w = dict(synth.WORKLOADS[a.workload])
 if a.count:
@@ -31,7 +32,8 @@ for r in range(a.reps):
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    ix.self_join_async(out, cnt)
+    for b in range(a.batches):
+        ix.self_join_async(out, cnt, b, a.batches)
     e.record()
     torch.cuda.synchronize()
     print(f"rep {r}: filter={ix.info().filter} tile_q={ix.info().tile_queries} pairs={int(cnt.item())} join_ms={s.elapsed_time(e):.2f} "
