@@ -55,8 +55,8 @@ def parse():
     p.add_argument("--no-sortidu", action="store_true")
     p.add_argument("--no-shortc", action="store_true")
     p.add_argument("--no-symmetric", action="store_true")
-    p.add_argument("--filter", type=int, default=2, choices=[0, 1, 2, 3],
-                   help="0 FP64 scan, 1 FP32 certified prefilter, 2 tcgen05 certified bound, 3 mma.sync bound")
+    p.add_argument("--filter", type=int, default=2, choices=[0, 1, 2],
+                   help="0 FP64 scan, 1 FP32 certified prefilter, 2 tcgen05 certified bound")
     p.add_argument("--mma-tiles", type=int, default=0, choices=[0, 1, 2],
                    help="filter 2: 128-query accumulator tiles per tcgen05 CTA (0 = library default, 1)")
     p.add_argument("--batch-size", type=int, default=0,
@@ -273,7 +273,7 @@ def main():
     # per-dimension counts of the FP64 stats scan (gj_join_stats)
     stats, mma_tests = None, None
     if not (args.profile or args.no_stats):
-        stats = ix0.counts(rank, world) if info.filter in (2, 3) else ix0.stats(rank, world)
+        stats = ix0.counts(rank, world) if info.filter == 2 else ix0.stats(rank, world)
         if info.filter == 2:
             mma_tests = ix0.mma_tests(rank, world) * (world if world > 1 else 1)
     info_k16 = info.mma_depth or None
@@ -372,15 +372,14 @@ def main():
     roof = None
     if stats is not None:
         scale = world if world > 1 else 1
-        if filt in (2, 3):
+        if filt == 2:
             # certified tensor-core bound: one n-dim dot product (2n flops) per
             # evaluated (unordered) candidate pair, on fp16 operands
             alg = 2.0 * n * stats["tests_evaluated"]
             # sustained figure: the join kernels run inside a ~100-200 ms step under the power cap
             peak = peaks.get("bf16_tflops_sustained", 1400.0)
             bound = "tensor"
-            kern = ("k_join_umma (tcgen05/TMEM fp16 bound + FP64 decision)" if filt == 2
-                    else "k_join_tc (mma.sync fp16 bound + FP64 decision)")
+            kern = "k_join_umma (tcgen05/TMEM fp16 bound + FP64 decision)"
             pnote = ("measured cuBLAS bf16 sustained, MEASURED_PEAKS.json" if "bf16_tflops_sustained" in peaks
                      else "fallback (B200_PROFILING.md): bf16 sustained ~1.4 PFLOP/s under the power cap") + \
                     "; fp16 has the same nominal dense rate"

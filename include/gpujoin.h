@@ -72,16 +72,16 @@ typedef struct {
                             1 = certified FP32 SHORTC prefilter (SIMT, packed f32x2)
                             2 = certified tensor-core bound on dense cell-pair blocks with
                                 tcgen05.mma (fp16 operands, fp32 accumulators in TMEM) (default)
-                            3 = the same bound with legacy mma.sync (baseline)
-                            2 and 3 fall back to 1, then 0, when the data's spread makes the
-                            bound uncertifiable.
+                            2 falls back to 1, then 0, when the data's spread makes the
+                            bound uncertifiable.  (Round 1's legacy mma.sync variant,
+                            filter 3, was removed: GJ_ERR_INVALID.)
                             gj_join_stats always runs the FP64 scan.                          */
-    int32_t mma_tiles;   /* filter 2 only: 128-query accumulator tiles per tcgen05 CTA that
-                            share every staged candidate block (UMMA M = 128 each):
-                            1 = query tiles of 128 points, 256-candidate blocks, two CTAs
-                            per SM (default); 2 = tiles of 256 points, 128-candidate blocks,
-                            one CTA per SM, half the candidate traffic per test;
-                            0 = default.  The pair set does not depend on it.               */
+    int32_t mma_tiles;   /* filter 2 only: queries per index tile, in units of 128:
+                            1 (or 0, default) = tiles of 128 queries, 2 = tiles of 256
+                            queries (each covered by two CTAs).  Every tcgen05 CTA holds one
+                            128-query A tile (UMMA M = 128), streams 128-candidate B blocks
+                            into two 128-column TMEM accumulator slots and runs two per
+                            SM.  The pair set does not depend on it.                         */
 } gj_options;
 
 /* Read-only description of a built index. */
@@ -97,7 +97,7 @@ typedef struct {
     int64_t n_tiles;      /* query tiles (<= tile_queries queries of one cell each) */
     double est_candidates;/* sum over queries of candidates before SORTIDU         */
     double build_ms;      /* device time of gj_build_index (CUDA events)           */
-    int32_t filter;       /* filter the join kernel actually runs (0..3, see gj_options) */
+    int32_t filter;       /* filter the join kernel actually runs (0..2, see gj_options) */
     float filter_threshold;  /* its rejection threshold (filter 2: in scaled units)      */
     double filter_margin; /* threshold / eps^2 - 1 (relative slack of the bound)          */
     int32_t tile_queries; /* queries per tile: 128, or 256 (filter 2 with mma_tiles = 2)  */

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpujoin.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["gj_capi.cu", "gj_index.cu", "gj_join.cu", "gj_join32.cu", "gj_join_tc.cu", "gj_join_umma.cu", "gj_radix.cu"]
+SOURCES = ["gj_capi.cu", "gj_index.cu", "gj_join.cu", "gj_join32.cu", "gj_join_umma.cu", "gj_radix.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
@@ -29,9 +29,14 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+# timing experiments only: extra nvcc flags (e.g. -DGJ_UMMA_EXPERIMENT=1) for an
+# A/B copy of the package built by tools/ab_prep.sh; never set for the product build
+EXTRA = os.environ.get("GJ_NVCC_EXTRA", "").split()
+
+
 def _compile(src: str, extra: list) -> tuple:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    r = subprocess.run([NVCC, *FLAGS, *extra, "-c", "-o", obj, src], capture_output=True, text=True)
+    r = subprocess.run([NVCC, *FLAGS, *EXTRA, *extra, "-c", "-o", obj, src], capture_output=True, text=True)
     return obj, r
 
 

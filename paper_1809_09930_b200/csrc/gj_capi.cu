@@ -196,7 +196,7 @@ int gj_build_index(const double* points, int64_t n_points, int32_t dim, double e
     ix.eps2 = eps * eps;
     ix.opt = o;
     ix.stream = (cudaStream_t)o.stream;
-    if (o.filter < 0 || o.filter > 3) { set_error("filter must be 0, 1, 2 or 3"); delete h; return GJ_ERR_INVALID; }
+    if (o.filter < 0 || o.filter > 2) { set_error("filter must be 0, 1 or 2"); delete h; return GJ_ERR_INVALID; }
     if (o.mma_tiles < 0 || o.mma_tiles > 2) { set_error("mma_tiles must be 0, 1 or 2"); delete h; return GJ_ERR_INVALID; }
     ix.filter = o.filter;
     const double* dX = points;

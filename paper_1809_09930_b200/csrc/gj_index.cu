@@ -203,12 +203,70 @@ __global__ void k_cells(const uint64_t* __restrict__ key, const uint32_t* __rest
     if (p == 0) cell_start[G] = (uint32_t)N;
 }
 
-// Adjacent non-empty cells (getAdjCells): one warp per cell, lanes split the
-// 3^k offsets (row-major over {-1,0,1}^k), each located by binary search in
-// the sorted id array.  FILL=false: counts + candidate sums (all adjacent
-// cells; and only cells with a larger index, for symmetric evaluation);
-// FILL=true: CSR in offset order (= increasing cell index) + the position of
-// the cell itself in its own list.
+// Adjacent non-empty cells (getAdjCells, Alg. 1 l.600; §5.6 l.896 "perform a
+// binary search to find the non-empty cells that exist in the index").
+//
+// The linear ids are row-major with the first indexed dimension most
+// significant (R9), so the non-empty cells sharing a coordinate prefix form a
+// contiguous range of the sorted id array.  One warp per cell: lane l takes
+// the l-th of the 3^m (m = min(k, 3)) offsets of the first m dimensions and
+// locates its prefix range by binary search; it then walks the remaining
+// offsets depth first, each child range found by binary search INSIDE its
+// parent's range, and an empty range prunes the whole subtree.  On sparse
+// grids (Songs-shaped data at k = 8: 3^8 = 6561 offsets per cell, few
+// non-empty) almost every subtree is pruned near the root, where the flat
+// enumeration paid one full-array binary search per offset; the results (and
+// their order) are the same.  FILL=false: counts + candidate sums (all
+// adjacent cells; and only cells with a larger index, for symmetric
+// evaluation); FILL=true: CSR in increasing cell index (lanes in prefix
+// order, each lane's walk in increasing id order) + the position of the cell
+// itself in its own list.
+__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* __restrict__ a, uint32_t lo, uint32_t hi,
+                                                    uint64_t key) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Depth-first walk of lane's prefix subtree; calls f(hit index) in increasing id order.
+template <typename F>
+__device__ __forceinline__ void adj_walk(const uint64_t* __restrict__ cell_id, uint32_t lo0, uint32_t hi0,
+                                         uint64_t base0, int m, int k, const int64_t* c, const int64_t* w,
+                                         const uint64_t* st, F&& f) {
+    uint32_t lo_s[kMaxK + 1], hi_s[kMaxK + 1];
+    uint64_t base_s[kMaxK + 1];
+    int64_t nx[kMaxK + 1];
+    int depth = m;
+    lo_s[m] = lo0;
+    hi_s[m] = hi0;
+    base_s[m] = base0;
+    if (m < k) nx[m] = c[m] - 1;
+    while (depth >= m) {
+        if (depth == k) {   // a leaf: the range holds exactly the one cell with this id
+            if (lo_s[k] < hi_s[k]) f(lo_s[k]);
+            --depth;
+            continue;
+        }
+        if (nx[depth] > c[depth] + 1) {
+            --depth;
+            continue;
+        }
+        const int64_t x = nx[depth]++;
+        if (x < 0 || x >= w[depth]) continue;
+        const uint64_t cb = base_s[depth] + (uint64_t)x * st[depth];
+        const uint32_t clo = lower_bound_u64(cell_id, lo_s[depth], hi_s[depth], cb);
+        const uint32_t chi = lower_bound_u64(cell_id, clo, hi_s[depth], cb + st[depth]);
+        if (clo == chi) continue;   // no non-empty cell below: prune the subtree
+        ++depth;
+        lo_s[depth] = clo;
+        hi_s[depth] = chi;
+        base_s[depth] = cb;
+        if (depth < k) nx[depth] = c[depth] - 1;
+    }
+}
+
 template <bool FILL>
 __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t* __restrict__ cell_start,
                            int64_t G, int k, const Meta* __restrict__ meta, uint32_t* __restrict__ cnt,
@@ -226,55 +284,49 @@ __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t*
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= G) return;
     const uint64_t lin = cell_id[g];
-    int64_t c[kMaxK];
-    for (int d = 0; d < k; ++d) c[d] = (int64_t)((lin / s_s[d]) % (uint64_t)s_w[d]);
-    int64_t total = 1;
-    for (int d = 0; d < k; ++d) total *= 3;
-    const uint64_t lo_id = cell_id[0], hi_id = cell_id[G - 1];
-    uint32_t found = 0, wpos = FILL ? off[g] : 0;
-    uint64_t csum = 0, casum = 0;
-    for (int64_t o0 = 0; o0 < total; o0 += 32) {
-        int64_t o = o0 + lane;
-        bool ok = o < total;
-        int64_t hit = -1;
-        if (ok) {
-            int64_t r = o;
-            uint64_t nl = 0;
-            for (int d = k - 1; d >= 0; --d) {
-                int64_t cd = c[d] + (r % 3) - 1;
-                r /= 3;
-                if (cd < 0 || cd >= s_w[d]) ok = false;
-                nl += (uint64_t)cd * s_s[d];
-            }
-            if (ok && nl >= lo_id && nl <= hi_id) {
-                int64_t lo = 0, hi = G;
-                while (lo < hi) {
-                    int64_t mid = (lo + hi) >> 1;
-                    if (cell_id[mid] < nl) lo = mid + 1; else hi = mid;
-                }
-                if (lo < G && cell_id[lo] == nl) hit = lo;
-            }
-        }
-        unsigned m = __ballot_sync(0xffffffffu, hit >= 0);
-        if (FILL) {
-            if (hit >= 0) {
-                const uint32_t at = wpos + __popc(m & ((1u << lane) - 1u));
-                nbr[at] = (uint32_t)hit;
-                if (hit == g) nbr_self[g] = at;
-            }
-            wpos += __popc(m);
-        } else {
-            found += __popc(m);
-            if (hit >= 0) {
-                const uint64_t sz = cell_start[hit + 1] - cell_start[hit];
-                csum += sz;
-                if (hit > g) casum += sz;
-            }
+    int64_t c[kMaxK], w[kMaxK];
+    uint64_t st[kMaxK];
+    for (int d = 0; d < k; ++d) {
+        w[d] = s_w[d];
+        st[d] = s_s[d];
+        c[d] = (int64_t)((lin / st[d]) % (uint64_t)w[d]);
+    }
+    // lane's prefix: offsets of the first m dims from the lane id, base 3, first dim most significant
+    const int m = k < 3 ? k : 3;
+    int np = 1;
+    for (int d = 0; d < m; ++d) np *= 3;
+    bool ok = lane < np;
+    uint64_t base = 0;
+    {
+        int r = lane, div = np / 3;
+        for (int d = 0; d < m; ++d) {
+            const int64_t x = c[d] + (ok ? (r / div) : 1) - 1;
+            r %= div;
+            div /= 3;
+            if (x < 0 || x >= w[d]) ok = false;
+            base += (uint64_t)(ok ? x : 0) * st[d];
         }
     }
+    uint32_t plo = 0, phi = 0;
+    if (ok) {
+        plo = lower_bound_u64(cell_id, 0, (uint32_t)G, base);
+        phi = lower_bound_u64(cell_id, plo, (uint32_t)G, base + st[m - 1]);
+    }
+    uint32_t found = 0;
+    uint64_t csum = 0, casum = 0;
+    if (plo < phi)
+        adj_walk(cell_id, plo, phi, base, m, k, c, w, st, [&](uint32_t hit) {
+            ++found;
+            if (!FILL) {
+                const uint64_t sz = cell_start[hit + 1] - cell_start[hit];
+                csum += sz;
+                if ((int64_t)hit > g) casum += sz;
+            }
+        });
     if (!FILL) {
 #pragma unroll
         for (int s = 16; s; s >>= 1) {
+            found += __shfl_xor_sync(0xffffffffu, found, s);
             csum += __shfl_xor_sync(0xffffffffu, csum, s);
             casum += __shfl_xor_sync(0xffffffffu, casum, s);
         }
@@ -283,7 +335,22 @@ __global__ void k_adjacent(const uint64_t* __restrict__ cell_id, const uint32_t*
             cand[g] = csum;
             cand_after[g] = casum;
         }
+        return;
     }
+    // exclusive scan of the lanes' counts: lane order = prefix order = id order
+    uint32_t incl = found;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+        if (lane >= s) incl += y;
+    }
+    uint32_t wpos = off[g] + incl - found;
+    if (plo < phi)
+        adj_walk(cell_id, plo, phi, base, m, k, c, w, st, [&](uint32_t hit) {
+            nbr[wpos] = hit;
+            if ((int64_t)hit == g) nbr_self[g] = wpos;
+            ++wpos;
+        });
 }
 
 __global__ void k_tile_count(const uint32_t* __restrict__ cell_start, int64_t G, uint32_t tq, uint32_t* __restrict__ nt) {
@@ -399,7 +466,7 @@ static bool fp32_threshold(Index* ix) {
     return fp32_threshold_from_spans(ix->eps, ix->n, spans, &ix->thr32, &ix->filter_margin) != 0;
 }
 
-// Threshold of the certified tensor-core bound (gj_join_umma.cu / gj_join_tc.cu;
+// Threshold of the certified tensor-core bound (gj_join_umma.cu;
 // DESIGN.md §"Tensor-core bound").  Operands: x^ = fp16(S (x - min)) for the
 // n coordinates, R2 = max ||x^||^2, K = padded MMA depth (n + 4 augmented
 // columns, rounded up to 16).  A query row carries (r_hi, r_lo, 1, 1) and a

@@ -65,7 +65,7 @@ struct Index {
     // device arrays
     double* pts = nullptr;           // [N][n_pad] reordered dims, sorted by (cell, u)
     float* pts32 = nullptr;          // [N][n_pad] fl32(x - min_j): input of the certified FP32 prefilter
-    int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tcgen05 bound, 3 mma.sync bound (+ FP64 decision)
+    int filter = 0;                  // 0 FP64 scan, 1 FP32 prefilter, 2 tcgen05 bound (+ FP64 decision)
     float thr32 = 0.f;               // FP32 prefilter rejection threshold (> eps^2, see fp32_threshold)
     float thr32_in = -1.f;           // FP32 certain-inside threshold (< eps^2): accepted without the FP64 test
     double filter_margin = 0;        // thr32 / eps^2 - 1
@@ -152,7 +152,6 @@ struct JoinParams {
     int k16;
     double thr16;
     uint32_t tile_q;                 // queries per index tile (128 or 256)
-    int debug;                       // timing experiments only (GJ_DEBUG_UMMA); 0 in production
 };
 
 // The query block of one CTA.  A CTA handles `qper` queries (128, or 256 in
@@ -232,7 +231,6 @@ int count_tests(const Index* ix, const JoinArgs& a, unsigned long long* d_out, c
 // FP32-prefilter variant (gj_join32.cu); kEmit / kCount only.
 int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // Tensor-core bound variants; kEmit / kCount only.
-int launch_join_tc(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);    // mma.sync (gj_join_tc.cu)
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);  // tcgen05 (gj_join_umma.cu)
 int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s);
 // Number of tile positions for (rank, world, batch, n_batches); sets first/step.

@@ -378,8 +378,6 @@ JoinParams join_params(const Index* ix) {
     p.k16 = ix->k16;
     p.thr16 = ix->thr16;
     p.tile_q = (uint32_t)ix->tile_q;
-    static const int dbg = [] { const char* e = getenv("GJ_DEBUG_UMMA"); return e ? atoi(e) : 0; }();
-    p.debug = dbg;
     return p;
 }
 
@@ -436,7 +434,6 @@ int launch_join(const Index* ix, JoinMode mode, const JoinArgs& a0, cudaStream_t
 
 static int launch_join_planned(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     if (ix->filter == 2 && mode != kStats) return launch_join_umma(ix, mode, a, s);
-    if (ix->filter == 3 && mode != kStats) return launch_join_tc(ix, mode, a, s);
     if (ix->filter == 1 && mode != kStats) return launch_join32(ix, mode, a, s);
     const Params p = join_params(ix);
     const int np = ix->n_pad;

@@ -3,9 +3,9 @@
 // FP64 decision of every surviving pair (B200-first variant of PAPER.md
 // Alg. 1 l.596-607; FP64 semantics unchanged).
 //
-// CTA = one producer warp, one MMA-issuer warp and 8 epilogue warps per
-// 128-query A tile of one cell (M = 128 TMEM lanes), candidates in blocks of
-// 128 rows, two accumulator slots, two CTAs per SM (see k_join_umma below).
+// CTA = one producer warp, one MMA-issuer warp and 4 x EPW epilogue warps per
+// 128-query A tile of one cell (M = 128 TMEM lanes); candidates in blocks of
+// BN = 256 (default) or 128 rows (see k_join_umma below for the roles).
 // The fp16 operands carry augmented columns so that every accumulator is
 // (T - ||q^ - c^||^2) / 2 (gj_index.cu tc_threshold_from): a pair survives the
 // bound iff its accumulator is > +0, and survivors are decided in FP64.
@@ -20,8 +20,17 @@
 namespace gj {
 namespace {
 
+// Timing experiments (tools/ab_prep.sh <name> <bits> builds an A/B copy with
+// -DGJ_UMMA_EXPERIMENT=<bits>; the product build has 0): 1 = the epilogue
+// releases each accumulator without reading it, 2 = no candidate loads,
+// 4 = accumulator reads without the sign test.
+#ifndef GJ_UMMA_EXPERIMENT
+#define GJ_UMMA_EXPERIMENT 0
+#endif
+constexpr int kExp = GJ_UMMA_EXPERIMENT;
+
 constexpr int kM = 128;         // queries per tile (UMMA M)
-constexpr int kN = 128;         // self-test GEMM width
+constexpr int kN = 128;         // candidates per block (UMMA N)
 // FP64 decision of one pair: the FP64 kernel's arithmetic (gj_join.cu).
 __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const double* __restrict__ b,
                                              int n_pad) {
@@ -69,120 +78,131 @@ __device__ __forceinline__ unsigned long long decide_batch(const JoinParams& P, 
     return 0ull;
 }
 
-// Per CTA: one 128-query A tile (M = 128 TMEM lanes) and a ring of
-// 128-candidate B blocks; TWO 128-column fp32 accumulator slots (the MMA of
-// block c + 1 runs while the epilogue reads block c), 8 epilogue warps
-// (TMEM lane quarter = warp % 4, column half = (warp - 2) / 4: 64 columns =
-// two tcgen05.ld.32x32b.x32 per warp and block) and TWO CTAs per SM (4 slots,
-// 16 epilogue warps, 2 MMA issuers per SM).  Measured on the block pipeline
-// alone (tools/micro/join_pipe, K = 48): 71 tests/clk/SM against 36 for four
-// CTAs with one slot each (the round-1 kernel) -- a slot must be re-filled
-// while another is read, and each block's TMEM read must be split over
-// enough warps that one warp's per-block latency chain stays short.
-constexpr int kBN = 128;                  // candidates per block (UMMA N)
-constexpr int kSlots = 2;                 // accumulator slots per CTA
-constexpr int kEpi = 8;                   // epilogue warps
-constexpr int kWarps = 2 + kEpi;          // 0 producer, 1 MMA issuer, 2..9 epilogue
-constexpr int kThreads = 32 * kWarps;
-constexpr int kCW = kBN / 2;              // accumulator columns per epilogue warp and block
-constexpr int kTCols = kSlots * kBN;      // TMEM columns per CTA (power of two)
-constexpr int kMaxWin = 512;              // adjacent cells handled per setup round
-constexpr int kSmemCap = 227 * 1024 / 2 - 2048;   // two CTAs per SM
-
-template <int KP>
-constexpr int umma_stages() {
-    // A tile + window arrays + survivor lists + barriers beside the ring
-    return (kSmemCap - 128 * KP * 2 - 3 * kMaxWin * 4 - kEpi * 64 * 8 - 512) / (kBN * KP * 2) < 8
-               ? (kSmemCap - 128 * KP * 2 - 3 * kMaxWin * 4 - kEpi * 64 * 8 - 512) / (kBN * KP * 2)
-               : 8;
+// Tensor memory: MT accumulator blocks of 128 query rows share every
+// candidate block (MT = 2: M = 2 x 128 per B operand, so the candidate stream
+// through L2 is halved per test).  An accumulator slot is MT x BN columns,
+// 256 / BN slots per CTA: MT = 1 uses 256 columns (two CTAs per SM, four
+// slots in flight per SM), MT = 2 all 512 (one CTA per SM).
+//
+// Epilogue: EPW warps per (A tile, 32-lane TMEM quarter), each reading BN / EPW
+// columns.  The accumulator read (4 B per candidate test against 2K MMA
+// flops) is as expensive as the MMA itself at K = 48, and TMEM read
+// throughput grows with the number of reading warps (tools/micro/tmem_ld_bw:
+// ~330 B/clk/SM with 8 warps, ~470 with 16), so MT = 1 runs EPW = 2 (16
+// epilogue warps per SM).
+constexpr int kMaxWin = 512;             // adjacent cells handled per setup round
+template <int MT, int EPW>
+constexpr int ws_warps() { return 2 + 4 * MT * EPW; }   // 0 producer, 1 MMA issuer, epilogue
+// CTAs per SM: two when a CTA's accumulator slots (MT x SL x BN columns) fit
+// in half of the SM's 512 TMEM columns.
+// (128-column accumulators: four CTAs per SM up to K = 48, three beyond, where
+// A + two ring stages no longer fit a quarter of the shared memory)
+template <int KP, int BN, int MT, int SL>
+constexpr int ws_ctas_per_sm() { return MT * SL * BN <= 128 ? (KP <= 48 ? 4 : 3) : (MT * SL * BN <= 256 ? 2 : 1); }
+template <int KP, int BN, int MT, int SL>
+constexpr int ws_budget_kb() {
+    return ws_ctas_per_sm<KP, BN, MT, SL>() == 4 ? 40
+           : ws_ctas_per_sm<KP, BN, MT, SL>() == 3 ? 64
+           : (ws_ctas_per_sm<KP, BN, MT, SL>() == 2 ? 96 : 196);
+}
+// Candidate ring depth: as many BN-row blocks as fit beside the A tiles in
+// ~100 KB (two CTAs per SM) or ~200 KB (one) of shared memory, at most 24.
+template <int KP, int BN, int MT, int SL>
+constexpr int ws_stages() {
+    return (ws_budget_kb<KP, BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2) < 24
+               ? (ws_budget_kb<KP, BN, MT, SL>() * 1024 - MT * 128 * KP * 2) / (BN * KP * 2)
+               : 24;
 }
 
-template <int KP>
-struct UmmaSmem {
-    alignas(128) __half a[kM * KP];                      // queries (A), canonical K-major layout
-    alignas(128) __half b[umma_stages<KP>()][kBN * KP];  // candidate ring (B)
-    uint64_t full[umma_stages<KP>()], empty[umma_stages<KP>()], accf[kSlots], acce[kSlots];
+template <int KP, int BN, int MT, int SL, int EPW>
+struct WsSmem {
+    alignas(128) __half a[MT][kM * KP];                           // queries (A), canonical K-major layout
+    alignas(128) __half b[ws_stages<KP, BN, MT, SL>()][BN * KP];   // candidate ring (B)
+    uint64_t full[ws_stages<KP, BN, MT, SL>()], empty[ws_stages<KP, BN, MT, SL>()], accf[SL], acce[SL];
     uint32_t tmem_base;
-    uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];     // window [r, s), blocks (bit 31: own cell)
-    uint2 sv[kEpi][64];                                  // per epilogue warp: staged survivors (qpos, cpos)
-    unsigned long long red[kWarps];
+    uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];          // window [r, s), blocks (bit 31: own cell)
+    uint2 sv[4 * MT * EPW][64];                               // per epilogue warp: staged survivors (qpos, cpos)
+    unsigned long long red[ws_warps<MT, EPW>()];
 };
 
-__device__ __forceinline__ void wait_parity(uint32_t mbar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAITP_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra WAITP_%=;\n\t}\n" ::"r"(mbar),
-        "r"(parity), "r"(0x989680u));
-}
-__device__ __forceinline__ void arrive_addr(uint32_t mbar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");
-}
-
-// Warp-specialised tcgen05 join (Alg. 1 l.596-607 with the certified
-// bound in front of the FP64 test).  Per CTA (128 queries of one cell): the
-// epilogue warps build the A tile (coordinates + augmented columns r_hi,
-// r_lo, 1, 1); all threads compute the SORTIDU windows of the adjacent cells
-// (thread per cell, union over the CTA's queries, §4.3); then
-//   producer : per 128-candidate block, one cp.async.bulk of the contiguous
-//              grouped-layout rows [8 floor(r/8) + 128 b, +128) into the ring
-//              (full/empty mbarriers, transaction bytes);
-//   MMA      : one thread, K/16 tcgen05.mma (M = N = 128) per block into
-//              accumulator slot c % 2; commits to empty[stage] and accf[slot];
-//   epilogue : 8 warps, each 32 rows x 64 columns of the slot: two
-//              tcgen05.ld, release the slot, AND of the 64 sign bits; the rare
-//              non-negative entries (survivors of the bound) inside [r, s) (and
-//              after the query in its own cell) are staged per warp and decided
-//              32 at a time in FP64, one pair per lane.
-template <int KP, int MODE, bool SYM>
-__global__ void __launch_bounds__(kThreads, 2) k_join_umma(JoinParams P, JoinArgs A) {
+// Warp-specialised tcgen05 join.  Per CTA (MT x 128 queries of one cell): the
+// epilogue warps build the A tiles (coordinates + augmented columns r_hi,
+// r_lo, 1, 1); all warps compute the SORTIDU windows of the adjacent cells
+// (thread per cell, union over the CTA's queries); then
+//   producer  : per BN-candidate block, one cp.async.bulk of the contiguous
+//               grouped-layout rows [8*floor(r/8) + BN b, +BN) into the ring
+//               (full/empty mbarriers, transaction bytes);
+//   MMA       : one thread, MT x K/16 tcgen05.mma per block (one per 128-query
+//               A tile, same B descriptor) into one accumulator slot, commits
+//               to empty[stage] and acc_full[slot];
+//   epilogue  : 4 x EPW warps per A tile (TMEM lane quarter = warp % 4, column
+//               part BN / EPW); tcgen05.ld, AND of the sign bits (survivor iff
+//               acc > +0), release the slot, then stage the rare survivors
+//               whose candidate lies in [r, s) (and after the query in its own
+//               cell) for a lane-parallel FP64 decision.
+template <int KP, int BN, int MT, int SL, int EPW, int MODE, bool SYM>
+__global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, BN, MT, SL>())
+    k_join_umma(JoinParams P, JoinArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    UmmaSmem<KP>& S = *reinterpret_cast<UmmaSmem<KP>*>(smem_raw);
-    constexpr int ST = umma_stages<KP>();
+    WsSmem<KP, BN, MT, SL, EPW>& S = *reinterpret_cast<WsSmem<KP, BN, MT, SL, EPW>*>(smem_raw);
+    constexpr int NE = 4 * MT * EPW;       // epilogue warps
+    constexpr int NW = ws_warps<MT, EPW>();
+    constexpr int NT = 32 * NW;
+    constexpr int QT = kM * MT;            // queries per CTA
+    constexpr uint32_t TCOLS = MT * SL * BN <= 128 ? 128 : (MT * SL * BN <= 256 ? 256 : 512);   // TMEM columns (power of 2)
     constexpr int KS = KP / 16;
-    constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, kBN);
+    constexpr int ST = ws_stages<KP, BN, MT, SL>();
+    constexpr int NACC = SL;
+    constexpr int CW = BN / EPW;           // accumulator columns per epilogue warp
+    constexpr int NL = CW / 32;            // 32-column TMEM loads per warp and block
+    constexpr uint32_t kIdesc = umma::idesc_f16_f32(kM, BN);
     constexpr uint32_t kSBO = KP * 16;
-    constexpr uint32_t kBlockBytes = kBN * KP * 2;
-    static_assert(ST >= 2, "candidate ring needs at least two stages");
-    static_assert(sizeof(UmmaSmem<KP>) <= kSmemCap, "shared memory");
+    constexpr uint32_t kBlockBytes = BN * KP * 2;
+    static_assert(NL >= 1 && NL <= 8, "epilogue columns per warp");
+    static_assert(ws_stages<KP, BN, MT, SL>() >= 1, "candidate ring needs at least one stage");
+    // TMEM loads in flight per wait: 4 (128 columns) when one warp reads a whole
+    // 256-column row (EPW = 1, 170 registers at two CTAs per SM), else 2
+    constexpr int NC = NL >= 8 ? 4 : (NL < 2 ? NL : 2);
+    constexpr int NMW = (NL + 1) / 2;       // 64-bit survivor mask words
 
-    const CtaTile ct = cta_tile(P, A, kM);
+    const CtaTile ct = cta_tile(P, A, QT);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int part = ct.part, split = ct.split;
     const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
+    const int nsub = (int)((nq + kM - 1) / kM);   // A tiles holding queries (1..MT)
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
-    if (warp == 1) umma::tmem_alloc(&S.tmem_base, kTCols);
+    if (warp == 1) umma::tmem_alloc(&S.tmem_base, TCOLS);
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
             umma::mbar_init(&S.full[i], 1);
             umma::mbar_init(&S.empty[i], 1);
         }
-        for (int i = 0; i < kSlots; ++i) {
+        for (int i = 0; i < NACC; ++i) {
             umma::mbar_init(&S.accf[i], 1);
-            umma::mbar_init(&S.acce[i], kEpi);
+            umma::mbar_init(&S.acce[i], 4 * EPW * nsub);
         }
         umma::mbar_fence_init();
     }
-    for (int row = tid - 64; row >= 0 && row < kM; row += 32 * kEpi) {   // A tile: thread = query row
+    for (int row = tid - 64; row >= 0 && row < QT; row += 32 * NE) {   // A tiles: thread = query row
+        const int sub = row >> 7, rr = row & (kM - 1);
         const bool valid = row < (int)nq;
-        unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a);
+        unsigned char* a_raw = reinterpret_cast<unsigned char*>(S.a[sub]);
         for (int kc = 0; kc < KP / 8; ++kc) {
-            union { uint4 u; __half h[8]; } cc;
-            cc.u = valid ? *reinterpret_cast<const uint4*>(P.pts16 + g16(q0 + row, kc * 8, KP)) : make_uint4(0, 0, 0, 0);
+            union { uint4 u; __half h[8]; } c;
+            c.u = valid ? *reinterpret_cast<const uint4*>(P.pts16 + g16(q0 + row, kc * 8, KP)) : make_uint4(0, 0, 0, 0);
             if (kc == KP / 8 - 1) {   // query-side augmented columns
-                query_aug(P.thr16, valid ? P.norm16[q0 + row] : 0.0, valid, cc.h[4], cc.h[5]);
-                cc.h[6] = __float2half(1.f);
-                cc.h[7] = __float2half(1.f);
+                query_aug(P.thr16, valid ? P.norm16[q0 + row] : 0.0, valid, c.h[4], c.h[5]);
+                c.h[6] = __float2half(1.f);
+                c.h[7] = __float2half(1.f);
             }
-            *reinterpret_cast<uint4*>(a_raw + umma::tile_off(row, kc * 8, KP)) = cc.u;
+            *reinterpret_cast<uint4*>(a_raw + umma::tile_off(rr, kc * 8, KP)) = c.u;
         }
     }
     unsigned long long npairs = 0;
-    if (SYM && part == 0 && tid < kM) {   // the self pair (q, q)
+    if (SYM && part == 0 && tid < QT) {   // the self pair (q, q)
         const bool active = tid < (int)nq;
         const uint32_t qid = P.orig[q0 + (active ? tid : 0)];
         if (MODE == kEmit) {
@@ -203,16 +223,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_join_umma(JoinParams P, JoinArg
     __syncthreads();
     umma::fence_after();
     const uint32_t tmem = S.tmem_base;
-    const uint32_t full0 = umma::smem_u32(&S.full[0]), empty0 = umma::smem_u32(&S.empty[0]);
-    const uint32_t accf0 = umma::smem_u32(&S.accf[0]), acce0 = umma::smem_u32(&S.acce[0]);
 
     const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
     const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
     uint32_t cnt = 0;   // blocks consumed so far (identical sequence in every role)
+    const int eidx = (warp - 2) >> 2;               // epilogue: (A tile, column part) of this warp
+    const int esub = eidx % MT, ecol = eidx / MT;
+    const int erow = kM * esub + 32 * (warp & 3) + lane;   // query row; TMEM lane = erow % 128
     for (uint32_t w0 = nb0; w0 < nb1; w0 += kMaxWin) {
         const int nwin = (int)min((uint32_t)kMaxWin, nb1 - w0);
-        for (int i = tid; i < nwin; i += kThreads) {   // windows of this round (thread per adjacent cell)
+        for (int i = tid; i < nwin; i += NT) {   // windows of this round (thread per adjacent cell)
             const uint32_t B = P.nbr[w0 + i];
             uint32_t r = P.cell_start[B], s = P.cell_start[B + 1];
             if (P.sortidu) {
@@ -239,113 +260,145 @@ __global__ void __launch_bounds__(kThreads, 2) k_join_umma(JoinParams P, JoinArg
             }
             S.wr[i] = r;
             S.ws[i] = s;
-            S.nbk[i] = (s > r ? (s - (r & ~7u) + kBN - 1) / kBN : 0u) | (diag ? 0x80000000u : 0u);
+            S.nbk[i] = (s > r ? (s - (r & ~7u) + BN - 1) / BN : 0u) | (diag ? 0x80000000u : 0u);
         }
         __syncthreads();
         if (warp == 0) {   // ---------------- producer
             if (lane == 0) {
                 uint32_t c = cnt;
                 for (int i = 0; i < nwin; ++i) {
-                    const uint32_t nb = S.nbk[i] & 0x7fffffffu;
-                    const __half* src = P.pts16 + (size_t)(S.wr[i] & ~7u) * KP;
-                    for (uint32_t bi = 0; bi < nb; ++bi, ++c, src += kBN * KP) {
+                    const uint32_t nb = S.nbk[i] & 0x7fffffffu, rb = S.wr[i] & ~7u;
+                    for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
                         const uint32_t st = c % ST, ph = (c / ST) & 1u;
-                        wait_parity(empty0 + 8 * st, ph ^ 1u);
+                        umma::mbar_wait(&S.empty[st], ph ^ 1u);
+                        if (kExp & 2) {   // timing experiment: no candidate loads
+                            umma::mbar_arrive(&S.full[st]);
+                            continue;
+                        }
                         umma::mbar_arrive_expect_tx(&S.full[st], kBlockBytes);
-                        umma::bulk_g2s(umma::smem_u32(S.b[st]), src, kBlockBytes, &S.full[st]);
+                        umma::bulk_g2s(umma::smem_u32(S.b[st]), P.pts16 + (size_t)(rb + bi * BN) * KP, kBlockBytes,
+                                       &S.full[st]);
                     }
                 }
             }
         } else if (warp == 1) {   // ---------------- MMA issuer
             if (lane == 0) {
-                const uint64_t adesc = umma::smem_desc(umma::smem_u32(S.a), 128, kSBO);
-                const uint64_t bdesc = umma::smem_desc(umma::smem_u32(S.b[0]), 128, kSBO);
                 uint32_t c = cnt;
-                uint32_t total = 0;
-                for (int i = 0; i < nwin; ++i) total += S.nbk[i] & 0x7fffffffu;
-                for (uint32_t e = 0; e < total; ++e, ++c) {
-                    const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c & 1u, aph = (c >> 1) & 1u;
-                    wait_parity(acce0 + 8 * ab, aph ^ 1u);
-                    wait_parity(full0 + 8 * st, ph);
-                    umma::fence_after();
-                    const uint64_t bd = bdesc + ((st * kBlockBytes) >> 4);
+                for (int i = 0; i < nwin; ++i) {
+                    const uint32_t nb = S.nbk[i] & 0x7fffffffu;
+                    for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
+                        const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c % NACC, aph = (c / NACC) & 1u;
+                        umma::mbar_wait(&S.acce[ab], aph ^ 1u);
+                        umma::mbar_wait(&S.full[st], ph);
+                        umma::fence_after();
+                        const uint32_t b_s = umma::smem_u32(S.b[st]);
 #pragma unroll
-                    for (int ks = 0; ks < KS; ++ks)
-                        umma::mma_f16(tmem + ab * kBN, adesc + (uint64_t)(ks * 16), bd + (uint64_t)(ks * 16), kIdesc,
-                                      ks > 0 ? 1u : 0u);
-                    umma::commit(&S.empty[st]);
-                    umma::commit(&S.accf[ab]);
+                        for (int sub = 0; sub < MT; ++sub) {
+                            if (sub >= nsub) break;
+                            const uint32_t a_s = umma::smem_u32(S.a[sub]);
+#pragma unroll
+                            for (int ks = 0; ks < KS; ++ks)
+                                umma::mma_f16(tmem + (uint32_t)((ab * MT + sub) * BN),
+                                              umma::smem_desc(a_s + ks * 256, 128, kSBO),
+                                              umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
+                        }
+                        umma::commit(&S.empty[st]);
+                        umma::commit(&S.accf[ab]);
+                    }
                 }
             }
-        } else {   // ---------------- epilogue
-            const int e = warp - 2;
-            const int erow = 32 * (warp & 3) + lane;            // query row = TMEM lane
-            const int ecol = e >> 2;                            // column half
+        } else if (esub < nsub) {   // ---------------- epilogue
+            uint32_t c = cnt;
             const uint32_t qpos = q0 + erow;
             const bool rvalid = erow < (int)nq;
-            const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(ecol * kCW);
+            const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
             const unsigned lt = (1u << lane) - 1u;
             // Survivors of the bound are staged per warp and decided 32 at a time
             // (one per lane), so a rare FP64 decision never holds the accumulator
             // pipeline for a full memory round trip per pair.
-            uint2* sv = S.sv[e];
+            uint2* sv = S.sv[warp - 2];
             uint32_t svn = 0;
-            uint32_t c = cnt;
             for (int i = 0; i < nwin; ++i) {
-                const uint32_t nb = S.nbk[i] & 0x7fffffffu;
+                const uint32_t nbw = S.nbk[i], nb = nbw & 0x7fffffffu, rb = S.wr[i] & ~7u;
+                const uint32_t wr = S.wr[i], wsd = S.ws[i];
+                const bool diag = (nbw >> 31) != 0;
                 for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
-                    const uint32_t ab = c & 1u;
-                    wait_parity(accf0 + 8 * ab, (c >> 1) & 1u);
+                    const uint32_t ab = c % NACC, aph = (c / NACC) & 1u;
+                    umma::mbar_wait(&S.accf[ab], aph);
                     umma::fence_after();
-                    uint32_t v[2][32];
-                    umma::tmem_ld32_nowait(tbase + ab * kBN, v[0]);
-                    umma::tmem_ld32_nowait(tbase + ab * kBN + 32, v[1]);
-                    umma::tmem_wait_ld();
-                    umma::fence_before();
-                    __syncwarp();
-                    if (lane == 0) arrive_addr(acce0 + 8 * ab);
-                    // sign bits: AND of the 64 accumulators (LOP3 chains)
-                    uint32_t t[16];
-#pragma unroll
-                    for (int k = 0; k < 16; ++k)
-                        t[k] = v[k >> 3][(4 * k) & 31] & v[k >> 3][(4 * k + 1) & 31] & v[k >> 3][(4 * k + 2) & 31] &
-                               v[k >> 3][(4 * k + 3) & 31];
-#pragma unroll
-                    for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-                        for (int k = 0; k < w; ++k) t[k] &= t[k + w];
-                    const bool any = rvalid && !(t[0] >> 31);   // rare: some accumulator > +0
-                    if (!__any_sync(0xffffffffu, any)) continue;
-                    unsigned long long m = 0ull;
-                    if (any) {
-#pragma unroll
-                        for (int x = 0; x < 2; ++x)
-#pragma unroll
-                            for (int y = 0; y < 32; ++y)
-                                if (!(v[x][y] >> 31)) m |= 1ull << (32 * x + y);
+                    const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN + ecol * CW);
+                    if (kExp & 1) {   // timing experiment: no accumulator reads
+                        __syncwarp();
+                        if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                        continue;
                     }
-                    const uint32_t wr = S.wr[i], wsd = S.ws[i];
-                    const bool diag = (S.nbk[i] >> 31) != 0;
-                    const uint32_t base = (wr & ~7u) + bi * kBN + ecol * kCW;
-                    while (__any_sync(0xffffffffu, m != 0ull)) {   // stage the survivors in [r, s)
-                        uint32_t cpos = 0;
-                        bool has = false;
-                        if (m) {
-                            const int bit = __ffsll((long long)m) - 1;
-                            m &= m - 1;
-                            cpos = base + bit;
-                            has = !(cpos < wr || cpos >= wsd || (diag && cpos <= qpos));
+                    // CW columns in chunks of NC x 32 (NC loads in flight, one wait); the
+                    // accumulator is released right after the last wait.  Survivors:
+                    // mask bit j of word w = column 64 w + j.
+                    unsigned long long mask[NMW];
+#pragma unroll
+                    for (int w = 0; w < NMW; ++w) mask[w] = 0ull;
+#pragma unroll
+                    for (int h = 0; h < NL / NC; ++h) {
+                        uint32_t v[NC][32];
+#pragma unroll
+                        for (int x = 0; x < NC; ++x) umma::tmem_ld32_nowait(tcol + 32 * (NC * h + x), v[x]);
+                        umma::tmem_wait_ld();
+                        if (h == NL / NC - 1) {
+                            umma::fence_before();
+                            __syncwarp();
+                            if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
                         }
-                        const unsigned hb = __ballot_sync(0xffffffffu, has);
-                        if (has) sv[svn + __popc(hb & lt)] = make_uint2(qpos, cpos);
-                        svn += __popc(hb);
-                        if (svn >= 32) {   // a full batch: one FP64 decision per lane
-                            __syncwarp();
-                            npairs += decide_batch<MODE, SYM>(P, A, sv, 32, lane);
-                            __syncwarp();
-                            if ((uint32_t)lane < svn - 32) sv[lane] = sv[32 + lane];
-                            svn -= 32;
-                            __syncwarp();
+                        if (kExp & 4) continue;   // timing experiment: reads only
+                        // sign bits: balanced AND tree (short dependency chains)
+                        uint32_t t[8 * NC];
+#pragma unroll
+                        for (int k = 0; k < 8 * NC; ++k) {
+                            const int e0 = 4 * k;
+                            t[k] = v[e0 / 32][e0 % 32] & v[(e0 + 1) / 32][(e0 + 1) % 32] &
+                                   v[(e0 + 2) / 32][(e0 + 2) % 32] & v[(e0 + 3) / 32][(e0 + 3) % 32];
+                        }
+#pragma unroll
+                        for (int w = 4 * NC; w >= 1; w >>= 1)
+#pragma unroll
+                            for (int k = 0; k < w; ++k) t[k] &= t[k + w];
+                        if (rvalid && !(t[0] >> 31)) {   // rare: some accumulator > +0
+#pragma unroll
+                            for (int x = 0; x < NC; ++x)
+#pragma unroll
+                                for (int y = 0; y < 32; ++y)
+                                    if (!(v[x][y] >> 31))
+                                        mask[(NC * h + x) >> 1] |= 1ull << (32 * ((NC * h + x) & 1) + y);
+                        }
+                    }
+                    unsigned long long anym = 0ull;
+#pragma unroll
+                    for (int w = 0; w < NMW; ++w) anym |= mask[w];
+                    if (!__any_sync(0xffffffffu, anym != 0ull)) continue;
+                    const uint32_t base = rb + bi * BN + ecol * CW;
+#pragma unroll
+                    for (int hh = 0; hh < NMW; ++hh) {
+                        unsigned long long m = mask[hh];
+                        while (__any_sync(0xffffffffu, m != 0ull)) {   // stage the survivors in [r, s)
+                            uint32_t cpos = 0;
+                            bool has = false;
+                            if (m) {
+                                const int bit = __ffsll((long long)m) - 1;
+                                m &= m - 1;
+                                cpos = base + 64 * hh + bit;
+                                has = !(cpos < wr || cpos >= wsd || (diag && cpos <= qpos));
+                            }
+                            const unsigned hb = __ballot_sync(0xffffffffu, has);
+                            if (has) sv[svn + __popc(hb & lt)] = make_uint2(qpos, cpos);
+                            svn += __popc(hb);
+                            if (svn >= 32) {   // a full batch: one FP64 decision per lane
+                                __syncwarp();
+                                npairs += decide_batch<MODE, SYM>(P, A, sv, 32, lane);
+                                __syncwarp();
+                                if ((uint32_t)lane < svn - 32) sv[lane] = sv[32 + lane];
+                                svn -= 32;
+                                __syncwarp();
+                            }
                         }
                     }
                 }
@@ -361,8 +414,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_join_umma(JoinParams P, JoinArg
     }
     umma::fence_before();
     __syncthreads();
-    if (warp == 1) umma::tmem_dealloc(tmem, kTCols);
-    if (A.mma_tests && tid == 0 && cnt) atomicAdd(A.mma_tests, (unsigned long long)cnt * kM * kBN);
+    if (warp == 1) umma::tmem_dealloc(tmem, TCOLS);
+    // executed accumulator entries (rows x columns of every block, padding included)
+    if (A.mma_tests && tid == 0 && cnt) atomicAdd(A.mma_tests, (unsigned long long)cnt * (kM * nsub) * BN);
 
     if (MODE == kCount) {
         unsigned long long x = npairs;
@@ -372,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_join_umma(JoinParams P, JoinArg
         __syncthreads();
         if (tid == 0) {
             unsigned long long t = 0;
-            for (int w = 0; w < kWarps; ++w) t += S.red[w];
+            for (int w = 0; w < NW; ++w) t += S.red[w];
             if (t) atomicAdd((unsigned long long*)A.count, t);
             if (part == 0) atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
         }
@@ -426,52 +480,83 @@ __global__ void __launch_bounds__(128) k_umma_selftest(const __half* __restrict_
     if (warp == 0) umma::tmem_dealloc(tmem, kN);
 }
 
-template <int KP, int MODE, bool SYM>
+template <int KP, int BN, int MT, int SL, int EPW, int MODE, bool SYM>
 int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
-    const size_t smem = sizeof(UmmaSmem<KP>);
+    using Smem = WsSmem<KP, BN, MT, SL, EPW>;
+    // two CTAs per SM (2 x 256 TMEM columns) or exactly one (512 columns),
+    // forced by > 114 KB of shared memory
+    constexpr int kCtas = ws_ctas_per_sm<KP, BN, MT, SL>();
+    const size_t smem = std::max<size_t>(sizeof(Smem), kCtas == 4 ? 40 * 1024
+                                                        : kCtas == 3 ? 58 * 1024
+                                                        : (kCtas == 2 ? 80 * 1024 : 120 * 1024));
+    static_assert(sizeof(Smem) <= 227 * 1024 / ws_ctas_per_sm<KP, BN, MT, SL>() - 1024, "shared memory");
     // the attribute is per device: one bit per device, set once
     static std::atomic<unsigned long long> attr_done{0};
     int dev = 0;
     GJ_CUDA(cudaGetDevice(&dev));
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load() & bit)) {
-        GJ_CUDA(cudaFuncSetAttribute((const void*)k_join_umma<KP, MODE, SYM>,
+        GJ_CUDA(cudaFuncSetAttribute((const void*)k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_done.fetch_or(bit);
     }
-    k_join_umma<KP, MODE, SYM><<<grid_ctas(a, (int)p.tile_q, kM), kThreads, smem, s>>>(p, a);
+    k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM>
+        <<<grid_ctas(a, (int)p.tile_q, kM * MT), 32 * ws_warps<MT, EPW>(), smem, s>>>(p, a);
     count_launch();
     GJ_CUDA(cudaGetLastError());
     return GJ_OK;
 }
 
-template <int KP>
+template <int KP, int BN, int MT, int SL, int EPW>
 int launch_umma(const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
     if (a.n_tiles <= 0) return GJ_OK;
-    if (mode == kEmit) return sym ? launch_umma_k<KP, kEmit, true>(p, a, s) : launch_umma_k<KP, kEmit, false>(p, a, s);
-    return sym ? launch_umma_k<KP, kCount, true>(p, a, s) : launch_umma_k<KP, kCount, false>(p, a, s);
+    if (mode == kEmit) return sym ? launch_umma_k<KP, BN, MT, SL, EPW, kEmit, true>(p, a, s)
+                                  : launch_umma_k<KP, BN, MT, SL, EPW, kEmit, false>(p, a, s);
+    return sym ? launch_umma_k<KP, BN, MT, SL, EPW, kCount, true>(p, a, s)
+               : launch_umma_k<KP, BN, MT, SL, EPW, kCount, false>(p, a, s);
+}
+
+// MMA depth dispatch; KMAX bounds the instantiated depths (a configuration
+// whose shared memory cannot hold a deeper ring is not instantiated beyond it).
+template <int BN, int MT, int SL, int EPW, int KMAX = 128>
+int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const JoinArgs& a, bool sym, cudaStream_t s) {
+    switch (ix->k16) {
+        case 16: return launch_umma<16, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 32: return launch_umma<32, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 48: return launch_umma<48, BN, MT, SL, EPW>(p, mode, a, sym, s);
+        case 64: if constexpr (KMAX >= 64) return launch_umma<64, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 80: if constexpr (KMAX >= 80) return launch_umma<80, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 96: if constexpr (KMAX >= 96) return launch_umma<96, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 112: if constexpr (KMAX >= 112) return launch_umma<112, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        case 128: if constexpr (KMAX >= 128) return launch_umma<128, BN, MT, SL, EPW>(p, mode, a, sym, s); break;
+        default: break;
+    }
+    set_error("tcgen05 join: MMA depth " + std::to_string(ix->k16) + " not instantiated for this configuration");
+    return GJ_ERR_INVALID;
 }
 
 }  // namespace
 
-// One 128-query A tile per CTA (index tiles of 256 queries, gj_options.mma_tiles
-// = 2, are covered by two CTAs each), MMA depth K = n + 4 rounded up to 16.
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
     const JoinParams p = join_params(ix);
     const bool sym = ix->opt.symmetric != 0;
-    switch (ix->k16) {
-        case 16: return launch_umma<16>(p, mode, a, sym, s);
-        case 32: return launch_umma<32>(p, mode, a, sym, s);
-        case 48: return launch_umma<48>(p, mode, a, sym, s);
-        case 64: return launch_umma<64>(p, mode, a, sym, s);
-        case 80: return launch_umma<80>(p, mode, a, sym, s);
-        case 96: return launch_umma<96>(p, mode, a, sym, s);
-        case 112: return launch_umma<112>(p, mode, a, sym, s);
-        case 128: return launch_umma<128>(p, mode, a, sym, s);
-        default: break;
-    }
-    set_error("tcgen05 join: MMA depth " + std::to_string(ix->k16) + " not instantiated");
-    return GJ_ERR_INVALID;
+    // A tiles per CTA = tile_q / 128.  MT = 1 (default): 128-candidate blocks,
+    // one 128-column accumulator per CTA and FOUR CTAs per SM (4 x 128 TMEM
+    // columns): four independent MMA -> epilogue pipelines per SM, so one CTA's
+    // epilogue (4 warps, 128 columns each) overlaps three others' MMAs.
+    // Alternatives measured slower on expo32 (DESIGN "What bounds the tcgen05
+    // join"): 256-candidate blocks with two CTAs per SM; two 128-column slots
+    // per CTA with 8 epilogue warps and two CTAs per SM (round 2: 185-196 vs
+    // 177-186 ms); 256-column slots, one CTA per SM, 16 epilogue warps.
+    if (ix->tile_q / kM == 2) return launch_umma_kp<128, 2, 2, 1>(ix, p, mode, a, sym, s);
+    // 128-candidate blocks with one accumulator per CTA: four CTAs per SM while
+    // A + two ring stages fit a quarter of the SM's shared memory (K <= 48),
+    // three up to K = 96 (3M x 64-d exponential, K = 80: 885 vs 899 ms with
+    // 256-candidate blocks and two CTAs per SM); K = 112, 128: 256-candidate
+    // blocks, two CTAs per SM
+    if (ix->k16 <= 48) return launch_umma_kp<128, 1, 1, 1, 48>(ix, p, mode, a, sym, s);
+    if (ix->k16 <= 96) return launch_umma_kp<128, 1, 1, 1, 96>(ix, p, mode, a, sym, s);
+    return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
 }
 
 int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s) {

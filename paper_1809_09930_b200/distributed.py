@@ -54,9 +54,10 @@ class Comm:
         return self.backend != "nccl" and t.is_cuda
 
     def broadcast(self, t, src: int = 0):
-        """In place; rank ``src``'s tensor is the value everywhere."""
+        """In place; rank ``src``'s tensor is the value everywhere.  Runs the
+        collective whenever a process group exists (world 1 included)."""
         import torch.distributed as dist
-        if self.world == 1:
+        if not self.on:
             return t
         if self._staged(t):
             h = t.cpu()
@@ -69,7 +70,7 @@ class Comm:
     def all_reduce(self, t, op: str = "sum"):
         """In place; ``op`` = "sum" or "max"."""
         import torch.distributed as dist
-        if self.world == 1:
+        if not self.on:
             return t
         rop = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX
         if self._staged(t):
@@ -82,7 +83,7 @@ class Comm:
 
     def barrier(self):
         import torch.distributed as dist
-        if self.world == 1:
+        if not self.on:
             return
         if self.backend == "nccl" and self.device is not None:
             dist.barrier(group=self.group, device_ids=[self.device.index])

@@ -66,7 +66,37 @@ def test_tcgen05_selftest_gemm():
     assert (D.double() - ref).abs().max().item() < 1e-5
 
 
-@pytest.mark.parametrize("filt", [0, 1, 2, 3])
+@pytest.mark.parametrize("kind", ["cancel", "mixed", "random"])
+def test_tcgen05_accumulation_error_within_model(kind):
+    """Empirical pin of the hardware model behind the certified bound
+    (gj_index.cu tc_threshold_from): fp16 products are exact in fp32 and the
+    fp32 accumulation of K terms errs by at most kappa * sum_k |a_k b_k|,
+    kappa = (K + 2) 2^-21.  The join kernel's tcgen05 path (gj_selftest_umma,
+    K = 32) on adversarial operands -- large terms that cancel, mixed
+    magnitudes, random -- against the exact fp64 products."""
+    from paper_1809_09930_b200 import gpujoin
+    g = np.random.default_rng({"cancel": 1, "mixed": 2, "random": 3}[kind])
+    if kind == "cancel":   # +-2^10 magnitudes summing to small results
+        A = g.choice([-1024.0, 1024.0, -1023.0, 1023.5], size=(128, 32))
+        B = g.choice([1.0, -1.0, 0.9990234375, 1.0009765625], size=(128, 32))
+    elif kind == "mixed":  # 2^-8 .. 2^8 terms in one sum
+        A = np.ldexp(g.choice([1.0, -1.0], size=(128, 32)), g.integers(-8, 9, size=(128, 32)))
+        B = np.ldexp(g.random((128, 32)) + 0.5, g.integers(-8, 9, size=(128, 32)))
+    else:
+        A, B = g.standard_normal((128, 32)) * 30, g.standard_normal((128, 32)) * 30
+    A16 = torch.from_numpy(A).half().cuda()
+    B16 = torch.from_numpy(B).half().cuda()
+    D = torch.full((128, 128), float("nan"), device="cuda")
+    gpujoin.selftest_umma(A16, B16, D)
+    a, b = A16.double().cpu().numpy(), B16.double().cpu().numpy()
+    exact = a @ b.T
+    mag = np.abs(a) @ np.abs(b).T
+    kappa = (32 + 2) * 2.0 ** -21
+    err = np.abs(D.double().cpu().numpy() - exact)
+    assert np.all(err <= kappa * mag + 1e-30), float(np.max(err / np.maximum(kappa * mag, 1e-30)))
+
+
+@pytest.mark.parametrize("filt", [0, 1, 2])
 @pytest.mark.parametrize("gen,count,dims,eps,k", [("exponential", 6000, 32, 0.08, 6), ("uniform", 3000, 16, 0.96, 6),
                                                    ("exponential", 2500, 64, 0.16, 6), ("songs_like", 4000, 90, 0.01, 6)])
 def test_filters_on_paper_shapes(filt, gen, count, dims, eps, k):
@@ -112,7 +142,7 @@ def test_pairs_equal_brute_force(gen, count, dims, eps, k):
 
 @pytest.mark.parametrize("reorder,sortidu,shortc,symmetric,filt",
                          [(r, s, c, y, f) for r in (0, 1) for s in (0, 1) for c in (0, 1) for y in (0, 1)
-                          for f in (0, 1, 2, 3)])
+                          for f in (0, 1, 2)])
 def test_every_flag_combination(reorder, sortidu, shortc, symmetric, filt):
     D = synth.exponential(2200, 24, seed=5)
     got, ix = gpu_pairs(D, 0.07, 4, reorder=reorder, sortidu=sortidu, shortc=shortc, symmetric=symmetric,
@@ -131,7 +161,7 @@ def _near_boundary_set(eps, n, m, rel, seed):
     return np.concatenate([base, base + dirs * eps * (1 + sign * rel)])
 
 
-@pytest.mark.parametrize("filt", [1, 2, 3])
+@pytest.mark.parametrize("filt", [1, 2])
 @pytest.mark.parametrize("rel", [1e-2, 1e-5, 1e-7, 3e-9])
 def test_certified_filters_near_the_boundary(rel, filt):
     # pairs just inside / just outside eps: a certified filter must never
@@ -144,6 +174,39 @@ def test_certified_filters_near_the_boundary(rel, filt):
     assert ixf.info().filter == filt
     A = {tuple(r) for r in a.tolist()}
     assert A == {tuple(r) for r in b.tolist()}
+    check(D, eps, a)
+
+
+def _near_enable_limit_set(eps, n, m, rel, seed, span_eps=46.0):
+    """Background points filling a box whose diagonal is ~span_eps * eps -- the
+    spread at which the tensor-core bound's slack T / (S eps)^2 - 1 sits just
+    under its 0.25 enable limit (the largest accumulation-error budget the
+    kernel ever runs with) -- plus m pairs at distance eps (1 +/- rel) placed in
+    the far corner of the box, where the operand norms (R2) are largest."""
+    rng = np.random.default_rng(seed)
+    side = span_eps * eps / np.sqrt(n)
+    bg = rng.random((2000, n)) * side
+    corner = np.stack([np.zeros(n), np.full(n, side)])
+    base = side - rng.random((m, n)) * 0.1 * side
+    dirs = -np.abs(rng.standard_normal((m, n)))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    sign = np.where(np.arange(m) % 2 == 0, 1.0, -1.0)[:, None]
+    return np.concatenate([bg, corner, base, base + dirs * eps * (1 + sign * rel)])
+
+
+@pytest.mark.parametrize("rel", [1e-5, 1e-7, 3e-9])
+def test_tensor_bound_at_its_enable_limit(rel):
+    """The certified tcgen05 bound where its error budget is largest: slack just
+    under the 0.25 enable limit (gj_index.cu tc_threshold_from), near-boundary
+    pairs at the largest operand norms.  Pair for pair equal to the FP64 scan
+    (filter 0) and to the oracle."""
+    eps, n = 0.05, 24
+    D = _near_enable_limit_set(eps, n, 1500, rel, seed=int(1 / rel) % 977)
+    a, ix2 = gpu_pairs(D, eps, 3, filter=2)
+    info = ix2.info()
+    assert info.filter == 2 and 0.18 <= info.filter_margin < 0.25, (info.filter, info.filter_margin)
+    b, _ = gpu_pairs(D, eps, 3, filter=0)
+    assert {tuple(r) for r in a.tolist()} == {tuple(r) for r in b.tolist()}
     check(D, eps, a)
 
 
@@ -160,7 +223,7 @@ def test_tensor_filters_at_the_dimension_limit(dims):
     assert len(got) > 1200
 
 
-@pytest.mark.parametrize("filt", [1, 2, 3])
+@pytest.mark.parametrize("filt", [1, 2])
 def test_filters_switch_off_when_they_cannot_certify(filt):
     # huge coordinate spread relative to eps: no certified filter is useful,
     # the index falls back to the FP64 scan (still exact).
@@ -204,7 +267,7 @@ def test_degenerate_inputs():
     # a dense duplicate cluster inside scattered points: one very heavy tile
     # (work-balanced split plans), for every filter
     D = np.concatenate([np.tile(np.array([[0.41] * 10]), (400, 1)), synth.uniform(600, 10, seed=6)])
-    for filt in (0, 1, 2, 3):
+    for filt in (0, 1, 2):
         got, ix = gpu_pairs(D, 0.3, 4, filter=filt)
         check(D, 0.3, got)
 

@@ -1,5 +1,5 @@
-"""A/B timing of two builds of the package (copies under abtest/<v>/, git-ignored):
-python tools/ab_join.py abtest/A [reps]"""
+"""A/B timing of builds of the package (copies under ab/<v>/ from tools/ab_prep.sh):
+python tools/ab_join.py ab/A [reps]  -- 3 result batches of the expo32 join, CUDA events"""
 import os, sys
 pkg = os.path.abspath(sys.argv[1])
 sys.path.insert(0, pkg)

@@ -1,7 +1,11 @@
-# tools/ab_prep.sh: copy the current package to abtest/$1 and build it there (for tools/ab_join.py)
+# tools/ab_prep.sh <name> [experiment bits]: copy the current package to ab/<name>
+# and build it there, optionally with -DGJ_UMMA_EXPERIMENT=<bits> (timing
+# experiments of the tcgen05 join, gj_join_umma.cu).  ab/ is git-ignored but
+# ships to the GPU box with gpurun; time two copies with tools/ab_join.py.
 set -e
 v=$1
-rm -rf abtest/$v && mkdir -p abtest/$v
-cp -r paper_1809_09930_b200 include abtest/$v/
-rm -rf abtest/$v/paper_1809_09930_b200/build abtest/$v/paper_1809_09930_b200/__pycache__ abtest/$v/paper_1809_09930_b200/libgpujoin.so
-(cd abtest/$v && python -c "import sys; sys.path.insert(0,'.'); import importlib; print(importlib.import_module('paper_1809_09930_b200._build').build(force=True))")
+bits=${2:-0}
+rm -rf ab/$v && mkdir -p ab/$v
+cp -r paper_1809_09930_b200 include ab/$v/
+rm -rf ab/$v/paper_1809_09930_b200/build ab/$v/paper_1809_09930_b200/__pycache__ ab/$v/paper_1809_09930_b200/libgpujoin.so
+(cd ab/$v && GJ_NVCC_EXTRA="-DGJ_UMMA_EXPERIMENT=$bits" python -c "import sys; sys.path.insert(0,'.'); import importlib; print(importlib.import_module('paper_1809_09930_b200._build').build(force=True))")

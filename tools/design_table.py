@@ -5,7 +5,7 @@ import sys
 
 b = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 rows = [json.loads(l) for l in open(sys.argv[2]) if l.strip()]
-names = {0: "FP64 scan", 1: "FP32 bound", 2: "tcgen05 bound", 3: "mma.sync bound"}
+names = {0: "FP64 scan", 1: "FP32 bound", 2: "tcgen05 bound"}
 
 
 def row(d):

@@ -33,7 +33,12 @@ def num(row, name, scale_units=True):
     i = col(name)
     if i is None or not row[i]:
         return None
-    v = float(row[i].replace(",", ""))
+    try:
+        v = float(row[i].replace(",", ""))
+    except ValueError:
+        return None
+    if v != v:   # nan: metric not collected for this launch
+        return None
     if scale_units:
         u = units[i].lower()
         v *= {"gbyte": 1e9, "mbyte": 1e6, "kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "usecond": 1e-6,
@@ -54,15 +59,19 @@ launches = []
 for row in rows:
     name = row[col("Kernel Name")]
     d = num(row, "gpu__time_duration.sum")
-    rd = num(row, "dram__bytes_read.sum") or 0.0
-    wr = num(row, "dram__bytes_write.sum") or 0.0
+    rd = num(row, "dram__bytes_read.sum")
+    wr = num(row, "dram__bytes_write.sum")
     launches.append({"kernel": name[:80], "duration_s": d, "dram_read": rd, "dram_write": wr,
                      **{k: num(row, m, False) for k, m in UTIL.items()}})
 T = sum(l["duration_s"] for l in launches) or 1.0
+ok = [l for l in launches if l["dram_read"] is not None and l["dram_write"] is not None]
+# launches whose DRAM counters were not collected are scaled in by duration
+scale = T / sum(l["duration_s"] for l in ok) if ok else None
 out = {"workload": workload, "filter": filt, "report": rep, "launches": len(launches),
-       "dram_bytes_per_join": sum(l["dram_read"] + l["dram_write"] for l in launches),
-       "dram_read_bytes": sum(l["dram_read"] for l in launches),
-       "dram_write_bytes": sum(l["dram_write"] for l in launches),
+       "launches_with_dram": len(ok),
+       "dram_bytes_per_join": sum(l["dram_read"] + l["dram_write"] for l in ok) * scale if ok else None,
+       "dram_read_bytes": sum(l["dram_read"] for l in ok) * scale if ok else None,
+       "dram_write_bytes": sum(l["dram_write"] for l in ok) * scale if ok else None,
        "ncu_duration_s": T}
 for k in UTIL:
     vals = [(l[k], l["duration_s"]) for l in launches if l[k] is not None]

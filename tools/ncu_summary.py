@@ -23,16 +23,24 @@ for w in want:
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
-hh = rows[1]
-data = rows[2:]
+hi = next(i for i, r in enumerate(rows) if "Source" in r and "Warp Stall Sampling (All Samples)" in r)
+hh = rows[hi]
+data = [r for r in rows[hi + 1:] if len(r) == len(hh)]   # first kernel section
 iS, iSrc, iE = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source"), hh.index("Instructions Executed")
-tot = sum(float(x[iS] or 0) for x in data) or 1.0
+def fnum(x):
+    try:
+        return float(x or 0)
+    except ValueError:
+        return 0.0
+
+
+tot = sum(fnum(x[iS]) for x in data) or 1.0
 cols = [c for c in hh if c.startswith("stall_") and "Not Issued" not in c]
-agg = {c: sum(float(x[hh.index(c)] or 0) for x in data) for c in cols}
+agg = {c: sum(fnum(x[hh.index(c)]) for x in data) for c in cols}
 print("# warp stall reasons (share of samples)")
 for c, s in sorted(agg.items(), key=lambda t: -t[1])[:8]:
     print(f"{c} = {100 * s / tot:.1f} %")
 print(f"# top {ntop} SASS sites by stall samples")
-for x in sorted(data, key=lambda x: -float(x[iS] or 0))[:ntop]:
-    st = sorted(((float(x[hh.index(c)] or 0), c) for c in cols), reverse=True)[:2]
-    print(f"{100 * float(x[iS]) / tot:5.1f}% {x[iSrc][:58]:58s} exec={x[iE]} {st[0][1]}/{st[1][1]}")
+for x in sorted(data, key=lambda x: -fnum(x[iS]))[:ntop]:
+    st = sorted(((fnum(x[hh.index(c)]), c) for c in cols), reverse=True)[:2]
+    print(f"{100 * fnum(x[iS]) / tot:5.1f}% {x[iSrc][:58]:58s} exec={x[iE]} {st[0][1]}/{st[1][1]}")
