@@ -687,6 +687,9 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaGetLastError());
     // 8. tiles, heaviest first (256 queries for the two-accumulator-tile tcgen05 kernel)
     ix->tile_q = ix->filter == 2 ? 128 * (ix->opt.mma_tiles == 2 ? 2 : 1) : kTileQ;
+    // FP32 filter on small cells (mean < 64 points): 32-query tiles, one warp
+    // each (gj_join32.cu k_join32w) instead of 128-query CTAs running mostly idle
+    if (ix->filter == 1 && N < 64 * G) ix->tile_q = 32;
     k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, (uint32_t)ix->tile_q, pos); count_launch();
     if ((rc = scan_u32(pos, pos, G, d_tot, s))) return rc;
     GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
