@@ -543,8 +543,15 @@ __global__ void k_norm16(int64_t N, int n, int k16, __half* __restrict__ pts16, 
 static int make_fp16(Index* ix, bool* ok) {
     cudaStream_t s = ix->stream;
     const Meta& m = ix->h_meta;
+    // dims carried by the MMA: the first n_mma of the REORDER order (all n by
+    // default; GJ_MMA_DIMS=<d> keeps only the d highest-variance dims, a timing
+    // experiment -- the bound then proves ||q - c|| over those dims > eps, which
+    // still implies the full distance does)
+    static const int env_dims = [] { const char* e = getenv("GJ_MMA_DIMS"); return e ? atoi(e) : 0; }();
+    const int n_mma = env_dims > 0 ? std::min(env_dims, ix->n) : ix->n;
+    ix->n_mma = n_mma;
     double ss = 0.0;
-    for (int t = 0; t < ix->n; ++t) {
+    for (int t = 0; t < n_mma; ++t) {
         const double sj = m.maxs[m.order[t]] - m.mins[m.order[t]];
         ss += sj * sj;
     }
@@ -553,7 +560,7 @@ static int make_fp16(Index* ix, bool* ok) {
     if (!(span < 1e300) || !(span > 0.0)) return GJ_OK;
     // S: power of two with S * span in [90, 180]: r, h, R2 and the sentinel fit fp16
     ix->tc_scale = std::ldexp(1.0, (int)std::floor(std::log2(180.0 / span)));
-    ix->k16 = (ix->n + 4 + 15) & ~15;
+    ix->k16 = (n_mma + 4 + 15) & ~15;
     if (ix->k16 > 128) return GJ_OK;   // n > 124: no MMA depth instantiated; fall back to the SIMT filters
     const int64_t N = ix->N;
     // rows padded to a multiple of 8 plus one 256-row block of zeros: block loads
@@ -565,9 +572,9 @@ static int make_fp16(Index* ix, bool* ok) {
     unsigned long long* d_r2 = nullptr;
     GJ_CUDA(pool_malloc(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
-    k_make16<<<blocks_for(N * ix->k16, 256), 256, 0, s>>>(ix->pts, N, ix->n, ix->n_pad, ix->k16, ix->tc_scale,
+    k_make16<<<blocks_for(N * ix->k16, 256), 256, 0, s>>>(ix->pts, N, n_mma, ix->n_pad, ix->k16, ix->tc_scale,
                                                           ix->meta, ix->pts16); count_launch();
-    k_norm16<<<blocks_for(N, 256), 256, 0, s>>>(N, ix->n, ix->k16, ix->pts16, ix->norm16, d_r2); count_launch();
+    k_norm16<<<blocks_for(N, 256), 256, 0, s>>>(N, n_mma, ix->k16, ix->pts16, ix->norm16, d_r2); count_launch();
     GJ_CUDA(cudaGetLastError());
     unsigned long long h_r2 = 0;
     GJ_CUDA(cudaMemcpyAsync(&h_r2, d_r2, sizeof(h_r2), cudaMemcpyDeviceToHost, s));
@@ -575,7 +582,7 @@ static int make_fp16(Index* ix, bool* ok) {
     GJ_CUDA(cudaStreamSynchronize(s));
     double R2;
     memcpy(&R2, &h_r2, sizeof(R2));
-    *ok = tc_threshold_from(ix->eps, ix->n, ix->k16, ix->tc_scale, R2, &ix->thr16, &ix->margin16) != 0;
+    *ok = tc_threshold_from(ix->eps, n_mma, ix->k16, ix->tc_scale, R2, &ix->thr16, &ix->margin16) != 0;
     if (!*ok) {
         GJ_CUDA(cudaFreeAsync(ix->pts16, s));
         GJ_CUDA(cudaFreeAsync(ix->norm16, s));
@@ -687,9 +694,6 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaGetLastError());
     // 8. tiles, heaviest first (256 queries for the two-accumulator-tile tcgen05 kernel)
     ix->tile_q = ix->filter == 2 ? 128 * (ix->opt.mma_tiles == 2 ? 2 : 1) : kTileQ;
-    // FP32 filter on small cells (mean < 64 points): 32-query tiles, one warp
-    // each (gj_join32.cu k_join32w) instead of 128-query CTAs running mostly idle
-    if (ix->filter == 1 && N < 64 * G) ix->tile_q = 32;
     k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, (uint32_t)ix->tile_q, pos); count_launch();
     if ((rc = scan_u32(pos, pos, G, d_tot, s))) return rc;
     GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

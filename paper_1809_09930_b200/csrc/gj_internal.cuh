@@ -71,7 +71,8 @@ struct Index {
     double filter_margin = 0;        // thr32 / eps^2 - 1
     __half* pts16 = nullptr;         // [N][k16] fp16(S (x - min_j)) + candidate-side augmented columns
     double* norm16 = nullptr;        // [N] ||fp16 coordinates||^2 (exact, fp64)
-    int k16 = 0;                     // MMA depth: n + 4 augmented columns, rounded up to 16
+    int k16 = 0;                     // MMA depth: n_mma + 4 augmented columns, rounded up to 16
+    int n_mma = 0;                   // leading (REORDER-order) dims carried by the MMA bound
     int tile_q = kTileQ;             // queries per tile: 128, or 256 for the M = 2 x 128 tcgen05 kernel
     double tc_scale = 1.0;           // S, a power of two
     double thr16 = 0.0;              // tensor-core bound threshold T (scaled units)

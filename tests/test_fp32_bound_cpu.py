@@ -37,26 +37,6 @@ def kernel_sums(q, c, mins):
     return out
 
 
-def kernel_sums_pairs(q, c, mins):
-    """The warp-per-tile kernel's order (gj_join32.cu k_join32w): packed f32x2
-    over pairs of consecutive dims -- two FMA chains (even / odd dims), the
-    running sum read as fl32(even + odd) after every 8 dims and at the end."""
-    ev, od = Fraction(0), Fraction(0)
-    out = []
-    n = len(q)
-    for j in range(n):
-        qj = f32(Fraction(float(np.float64(q[j]) - np.float64(mins[j]))))
-        cj = f32(Fraction(float(np.float64(c[j]) - np.float64(mins[j]))))
-        t = f32(cj - qj)                                                   # FADD2 (c + (-q))
-        if j % 2 == 0:
-            ev = f32(t * t + ev)                                           # FFMA2
-        else:
-            od = f32(t * t + od)
-        if (j + 1) % 8 == 0 or j == n - 1:
-            out.append(f32(ev + od))
-    return out
-
-
 @pytest.fixture(scope="module", autouse=True)
 def _build():
     import __graft_entry__
@@ -84,7 +64,7 @@ def test_no_inside_pair_is_rejected(n, eps, span, shift):
         d2 = sum((Fraction(float(a)) - Fraction(float(b))) ** 2 for a, b in zip(q, c))
         if d2 > Fraction(eps) ** 2:
             continue
-        for s in kernel_sums(q, c, mins) + kernel_sums_pairs(q, c, mins):
+        for s in kernel_sums(q, c, mins):
             assert s <= thr
 
 
@@ -112,10 +92,8 @@ def test_no_outside_pair_is_accepted_without_fp64(n, eps, span, shift):
         c = np.clip(q + v * eps * rel, shift, shift + span)
         d2 = sum((Fraction(float(a)) - Fraction(float(b))) ** 2 for a, b in zip(q, c))
         final = kernel_sums(q, c, mins)[-1]
-        final_w = kernel_sums_pairs(q, c, mins)[-1]
         if d2 >= lim * lim:
             assert final > T, "an outside / boundary pair would skip the FP64 test"
-            assert final_w > T, "(warp-per-tile order) an outside pair would skip the FP64 test"
         elif d2 <= (Fraction(eps) * Fraction(999, 1000)) ** 2 * Fraction(1001, 1000):
             n_inside_ok += final <= T
     assert n_inside_ok > 30

@@ -2,8 +2,11 @@
 share run one after another on ONE GPU (index build, estimator, join of the
 rank's tiles), to project entity-partitioned scaling before 8 GPUs are
 available: python tools/scaling_projection.py [--workload expo32]
-The projection is max over ranks of (build + estimate + join); NCCL broadcast
-and all-reduce are not included (measured separately on NVLink)."""
+Each rank's phase times are the MEDIAN of --reps runs; the projected step is
+max over ranks of (build + estimate + join) plus, for world > 1, the two
+collectives of the step modelled from the measured NVLink figures of
+B200_PROFILING.md: the NCCL broadcast of D (|D| n 8 bytes at the 8-rank
+725 GB/s bus bandwidth) and the 8-byte count all-reduce (~0.03 ms)."""
 import argparse
 import json
 import os
@@ -17,7 +20,8 @@ from paper_1809_09930_b200 import Index, num_batches  # noqa: E402
 
 p = argparse.ArgumentParser()
 p.add_argument("--workload", default="expo32")
-p.add_argument("--reps", type=int, default=3)
+p.add_argument("--reps", type=int, default=5)
+p.add_argument("--bus-gbs", type=float, default=725.0, help="NVLink bus bandwidth for the broadcast model")
 a = p.parse_args()
 w = synth.WORKLOADS[a.workload]
 D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
@@ -27,7 +31,7 @@ res = {}
 for world in (1, 2, 4, 8):
     per_rank = []
     for rank in range(world):
-        best = None
+        runs = []
         for _ in range(a.reps):
             ev[0].record()
             ix = Index(D, w["eps"], w["k"])
@@ -53,13 +57,15 @@ for world in (1, 2, 4, 8):
             t = [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
             ix.free()
             del out
-            if best is None or sum(t) < sum(best):
-                best = t
-        per_rank.append(best)
-    step = max(sum(t) for t in per_rank)
-    res[world] = {"step_ms": step, "per_rank_ms": per_rank}
+            runs.append(t)
+        runs.sort(key=sum)
+        per_rank.append(runs[len(runs) // 2])   # median step
+    coll = 0.0 if world == 1 else w["count"] * w["dims"] * 8 / (a.bus_gbs * 1e9) * 1e3 + 0.03
+    step = max(sum(t) for t in per_rank) + coll
+    res[world] = {"step_ms": step, "collectives_ms": coll, "per_rank_ms": per_rank}
     eff = res[1]["step_ms"] / (world * step)
+    res[world]["efficiency"] = eff
     print(f"world {world}: max-over-ranks step {step:.1f} ms (build {per_rank[0][0]:.1f}, estimate {per_rank[0][1]:.1f}, "
-          f"join {max(t[2] for t in per_rank):.1f} max / {min(t[2] for t in per_rank):.1f} min) -> efficiency {eff:.2f}",
-          flush=True)
+          f"join {max(t[2] for t in per_rank):.1f} max / {min(t[2] for t in per_rank):.1f} min, collectives "
+          f"{coll:.2f}) -> efficiency {eff:.2f}", flush=True)
 print(json.dumps({"workload": a.workload, "projection": res}))
