@@ -13,16 +13,21 @@
 // streams B's candidates through shared memory in coalesced double2 chunks;
 // every thread tests its query against every staged candidate:
 //   SORTIDU (§4.3): the staged range is the union of the tile's u-windows,
-//     found by binary search in B's u-sorted run; each thread then applies
-//     its own window |p(u) - q(u)| <= eps exactly.
+//     found by binary search in B's u-sorted run.  In emit / count mode every
+//     thread tests every candidate of that union (a candidate outside its own
+//     query's window is farther than eps on u alone, so the distance test
+//     rejects it: same pairs); stats mode additionally applies each query's
+//     own window |p(u) - q(u)| <= eps so the work counters are the paper's.
 //   SHORTC (§4.4): the squared-distance sum is accumulated in dimension
 //     order (highest variance first after REORDER) and abandoned as soon as
 //     it exceeds eps^2 (checked every 4 dims; stats mode: every dim).
 // Pairs are emitted with one warp-aggregated atomic per candidate that hit in
 // at least one lane (ballot -> leader atomicAdd -> shfl -> per-lane store).
 //
-// No tensor cores: the candidate work is a filtered gather with a
-// data-dependent early exit, not a dense contraction (north_star).
+// This is filter 0, the FP64 reference scan of the north_star; the default
+// (filter 2, gj_join_umma.cu) puts a certified tcgen05 bound in front of the
+// same FP64 test because on the paper's workloads the gather is a contiguous
+// range of a cell-sorted array, i.e. a dense block.
 #include <stdlib.h>
 
 #include <algorithm>
