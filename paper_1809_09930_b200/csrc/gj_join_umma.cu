@@ -28,6 +28,10 @@ namespace {
 #define GJ_UMMA_EXPERIMENT 0
 #endif
 constexpr int kExp = GJ_UMMA_EXPERIMENT;
+// bit 64: clock64 phase counters per role (tools/experiments/umma_prof.py reads
+// them through gj_debug_umma_prof, which only the experiment build exports)
+constexpr bool kProf = (kExp & 64) != 0;
+__device__ unsigned long long g_umma_prof[16];
 
 constexpr int kM = 128;         // queries per tile (UMMA M)
 constexpr int kN = 128;         // candidates per block (UMMA N)
@@ -283,14 +287,18 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
             }
         } else if (warp == 1) {   // ---------------- MMA issuer
             if (lane == 0) {
+                unsigned long long mp[5] = {0, 0, 0, 0, 0};   // wait acce, wait full, mma issue, commits, blocks
                 uint32_t c = cnt;
                 for (int i = 0; i < nwin; ++i) {
                     const uint32_t nb = S.nbk[i] & 0x7fffffffu;
                     for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
                         const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c % NACC, aph = (c / NACC) & 1u;
+                        const long long m0 = kProf ? clock64() : 0;
                         umma::mbar_wait(&S.acce[ab], aph ^ 1u);
+                        const long long m1 = kProf ? clock64() : 0;
                         umma::mbar_wait(&S.full[st], ph);
                         umma::fence_after();
+                        const long long m2 = kProf ? clock64() : 0;
                         const uint32_t b_s = umma::smem_u32(S.b[st]);
 #pragma unroll
                         for (int sub = 0; sub < MT; ++sub) {
@@ -302,10 +310,16 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                                               umma::smem_desc(a_s + ks * 256, 128, kSBO),
                                               umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
                         }
+                        const long long m3 = kProf ? clock64() : 0;
                         umma::commit(&S.empty[st]);
                         umma::commit(&S.accf[ab]);
+                        if (kProf) {
+                            const long long m4 = clock64();
+                            mp[0] += m1 - m0; mp[1] += m2 - m1; mp[2] += m3 - m2; mp[3] += m4 - m3; mp[4] += 1;
+                        }
                     }
                 }
+                if (kProf) for (int k = 0; k < 5; ++k) atomicAdd(&g_umma_prof[8 + k], mp[k]);
             }
         } else if (esub < nsub) {   // ---------------- epilogue
             uint32_t c = cnt;
@@ -318,14 +332,19 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
             // pipeline for a full memory round trip per pair.
             uint2* sv = S.sv[warp - 2];
             uint32_t svn = 0;
+            unsigned long long pr[4] = {0, 0, 0, 0};   // wait accf, reads -> release, after release, blocks
+            unsigned long long rare_cyc = 0, rare_n = 0;
             for (int i = 0; i < nwin; ++i) {
                 const uint32_t nbw = S.nbk[i], nb = nbw & 0x7fffffffu, rb = S.wr[i] & ~7u;
                 const uint32_t wr = S.wr[i], wsd = S.ws[i];
                 const bool diag = (nbw >> 31) != 0;
                 for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
                     const uint32_t ab = c % NACC, aph = (c / NACC) & 1u;
+                    const long long p0 = kProf ? clock64() : 0;
                     umma::mbar_wait(&S.accf[ab], aph);
                     umma::fence_after();
+                    long long p1 = kProf ? clock64() : 0;
+                    if (kProf) pr[0] += p1 - p0;
                     const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN + ecol * CW);
                     if (kExp & 1) {   // timing experiment: no accumulator reads
                         __syncwarp();
@@ -348,6 +367,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                             umma::fence_before();
                             __syncwarp();
                             if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
+                            if (kProf) { const long long t = clock64(); pr[1] += t - p1; p1 = t; }
                         }
                         if (kExp & 4) continue;   // timing experiment: reads only
                         // sign bits: balanced AND tree (short dependency chains)
@@ -374,7 +394,12 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                     unsigned long long anym = 0ull;
 #pragma unroll
                     for (int w = 0; w < NMW; ++w) anym |= mask[w];
-                    if (!__any_sync(0xffffffffu, anym != 0ull)) continue;
+                    const bool rare_b = __any_sync(0xffffffffu, anym != 0ull);
+                    if (kProf) {
+                        pr[3] += 1;
+                        if (!rare_b) pr[2] += clock64() - p1;
+                    }
+                    if (!rare_b) continue;
                     const uint32_t base = rb + bi * BN + ecol * CW;
 #pragma unroll
                     for (int hh = 0; hh < NMW; ++hh) {
@@ -401,11 +426,17 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                             }
                         }
                     }
+                    if (kProf) { const long long t = clock64(); pr[2] += t - p1; rare_cyc += t - p1; ++rare_n; }
                 }
             }
             if (svn) {   // the rest of this round's survivors
                 __syncwarp();
                 npairs += decide_batch<MODE, SYM>(P, A, sv, svn, lane);
+            }
+            if (kProf && lane == 0) {
+                for (int k = 0; k < 4; ++k) atomicAdd(&g_umma_prof[k], pr[k]);
+                atomicAdd(&g_umma_prof[4], rare_cyc);
+                atomicAdd(&g_umma_prof[5], rare_n);
             }
         }
         // every role walked the same block sequence
@@ -554,6 +585,8 @@ int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStre
     // three up to K = 96 (3M x 64-d exponential, K = 80: 885 vs 899 ms with
     // 256-candidate blocks and two CTAs per SM); K = 112, 128: 256-candidate
     // blocks, two CTAs per SM
+    // (four CTAs per SM with 8 epilogue warps of 64 columns each does not fit:
+    // 48 registers per thread cannot hold a 32-column TMEM load, ptxas C7602)
     if (ix->k16 <= 48) return launch_umma_kp<128, 1, 1, 1, 48>(ix, p, mode, a, sym, s);
     if (ix->k16 <= 96) return launch_umma_kp<128, 1, 1, 1, 96>(ix, p, mode, a, sym, s);
     return launch_umma_kp<256, 1, 1, 2>(ix, p, mode, a, sym, s);
@@ -568,3 +601,13 @@ int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s) {
 }
 
 }  // namespace gj
+
+#if GJ_UMMA_EXPERIMENT & 64
+// experiment build only: read and reset the phase counters
+extern "C" __attribute__((visibility("default"))) int gj_debug_umma_prof(unsigned long long* out) {
+    if (cudaMemcpyFromSymbol(out, gj::g_umma_prof, sizeof(gj::g_umma_prof)) != cudaSuccess) return -2;
+    static const unsigned long long zero[16] = {};
+    cudaMemcpyToSymbol(gj::g_umma_prof, zero, sizeof(zero));
+    return 0;
+}
+#endif

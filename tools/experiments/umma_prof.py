@@ -1,9 +1,9 @@
-"""Phase breakdown of the tcgen05 join (experiment build with -DGJ_UMMA_EXPERIMENT=64):
-python tools/umma_prof.py <package dir> -- prints per-block cycles of each role's phases."""
+"""Phase breakdown of the tcgen05 join (experiment build: tools/ab_prep.sh prof 64):
+python tools/experiments/umma_prof.py ab/prof -- per-block cycles of each role's phases."""
 import ctypes, os, sys
 pkg = os.path.abspath(sys.argv[1])
 sys.path.insert(0, pkg)
-sys.path.insert(1, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(1, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import synth
 from paper_1809_09930_b200 import Index, gpujoin
@@ -24,12 +24,10 @@ e.record()
 torch.cuda.synchronize()
 L.gj_debug_umma_prof(buf)
 v = list(buf)
-blocks = v[10]
-warp_blocks = blocks * 8
-print(f"join ms {s.elapsed_time(e):.1f} pairs {int(cnt.item())} blocks {blocks}")
-names = ["wait accf", "ld+release", "fast path", "rare path (incl decide)", "decide"]
-for k, nm in enumerate(names):
-    print(f"  epilogue {nm:28s}: {v[k] / warp_blocks:8.1f} cyc per warp-block")
-print(f"  rare warp-blocks: {v[5] / warp_blocks * 100:.2f} %   decides: {v[6]}  ({v[4] / max(1, v[6]):.0f} cyc each)")
-print(f"  MMA wait acce {v[8] / blocks:.1f}  wait full {v[9] / blocks:.1f}  mma issue {v[12] / blocks:.1f}  "
-      f"commits {v[13] / blocks:.1f}  total/block {v[11] / blocks:.1f} cyc")
+blocks = v[12]
+wb = v[3]
+print(f"join ms {s.elapsed_time(e):.1f} pairs {int(cnt.item())} blocks {blocks} warp-blocks {wb}")
+print(f"  epilogue per warp-block: wait accf {v[0] / wb:.1f}  TMEM reads -> release {v[1] / wb:.1f}  "
+      f"after release {v[2] / wb:.1f} cyc;  rare {v[5] / wb * 100:.2f} % of warp-blocks, {v[4] / max(1, v[5]):.0f} cyc each")
+print(f"  MMA issuer per block: wait release {v[8] / blocks:.1f}  wait loads {v[9] / blocks:.1f}  "
+      f"issue {v[10] / blocks:.1f}  commits {v[11] / blocks:.1f} cyc")
