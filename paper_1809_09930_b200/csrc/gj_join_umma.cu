@@ -122,7 +122,7 @@ template <int KP, int BN, int MT, int SL, int EPW>
 struct WsSmem {
     alignas(128) __half a[MT][kM * KP];                           // queries (A), canonical K-major layout
     alignas(128) __half b[ws_stages<KP, BN, MT, SL>()][BN * KP];   // candidate ring (B)
-    uint64_t full[ws_stages<KP, BN, MT, SL>()], empty[ws_stages<KP, BN, MT, SL>()], accf[SL], acce[SL];
+    uint64_t full[ws_stages<KP, BN, MT, SL>()], empty[ws_stages<KP, BN, MT, SL>()], accf[2 * SL], acce[2 * SL];
     uint32_t tmem_base;
     uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];          // window [r, s), blocks (bit 31: own cell)
     uint2 sv[4 * MT * EPW][64];                               // per epilogue warp: staged survivors (qpos, cpos)
@@ -168,6 +168,17 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
     // 256-column row (EPW = 1, 170 registers at two CTAs per SM), else 2
     constexpr int NC = NL >= 8 ? 4 : (NL < 2 ? NL : 2);
     constexpr int NMW = (NL + 1) / 2;       // 64-bit survivor mask words
+    // Half-split accumulator (timing experiment, -DGJ_UMMA_HALVES=1; default
+    // shape only): each block's MMA is issued as two N = 64 halves, each with
+    // its own full / empty barrier pair, so the next block's first half is
+    // computed while the epilogue still reads the second half of this one.
+    // Parity-green but not faster (DESIGN "What bounds the tcgen05 join").
+#ifndef GJ_UMMA_HALVES
+#define GJ_UMMA_HALVES 0   // measured 176-188 vs 172-179 ms on expo32: off
+#endif
+    constexpr bool HS = GJ_UMMA_HALVES && MT == 1 && SL == 1 && EPW == 1 && BN == 128 && NL / NC == 2;
+    constexpr int NBAR = HS ? 2 : NACC;
+    constexpr uint32_t kIdescH = umma::idesc_f16_f32(kM, BN / 2);
 
     const CtaTile ct = cta_tile(P, A, QT);
     if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
             umma::mbar_init(&S.full[i], 1);
             umma::mbar_init(&S.empty[i], 1);
         }
-        for (int i = 0; i < NACC; ++i) {
+        for (int i = 0; i < NBAR; ++i) {
             umma::mbar_init(&S.accf[i], 1);
             umma::mbar_init(&S.acce[i], 4 * EPW * nsub);
         }
@@ -294,6 +305,26 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                     for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
                         const uint32_t st = c % ST, ph = (c / ST) & 1u, ab = c % NACC, aph = (c / NACC) & 1u;
                         const long long m0 = kProf ? clock64() : 0;
+                        if (HS) {   // two N = 64 halves, each behind its own release
+                            umma::mbar_wait(&S.full[st], ph);
+                            const uint32_t b_s = umma::smem_u32(S.b[st]);
+                            const uint32_t a_s = umma::smem_u32(S.a[0]);
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf) {
+                                umma::mbar_wait(&S.acce[hf], (c & 1u) ^ 1u);
+                                umma::fence_after();
+#pragma unroll
+                                for (int ks = 0; ks < KS; ++ks)
+                                    umma::mma_f16(tmem + (uint32_t)(hf * (BN / 2)),
+                                                  umma::smem_desc(a_s + ks * 256, 128, kSBO),
+                                                  umma::smem_desc(b_s + ks * 256 + hf * 8 * kSBO, 128, kSBO), kIdescH,
+                                                  ks > 0 ? 1u : 0u);
+                                umma::commit(&S.accf[hf]);
+                            }
+                            umma::commit(&S.empty[st]);
+                            if (kProf) { mp[2] += clock64() - m0; mp[4] += 1; }
+                            continue;
+                        }
                         umma::mbar_wait(&S.acce[ab], aph ^ 1u);
                         const long long m1 = kProf ? clock64() : 0;
                         umma::mbar_wait(&S.full[st], ph);
@@ -341,12 +372,14 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                 for (uint32_t bi = 0; bi < nb; ++bi, ++c) {
                     const uint32_t ab = c % NACC, aph = (c / NACC) & 1u;
                     const long long p0 = kProf ? clock64() : 0;
-                    umma::mbar_wait(&S.accf[ab], aph);
-                    umma::fence_after();
+                    if (!HS) {
+                        umma::mbar_wait(&S.accf[ab], aph);
+                        umma::fence_after();
+                    }
                     long long p1 = kProf ? clock64() : 0;
                     if (kProf) pr[0] += p1 - p0;
                     const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN + ecol * CW);
-                    if (kExp & 1) {   // timing experiment: no accumulator reads
+                    if ((kExp & 1) && !HS) {   // timing experiment: no accumulator reads
                         __syncwarp();
                         if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
                         continue;
@@ -360,10 +393,19 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
 #pragma unroll
                     for (int h = 0; h < NL / NC; ++h) {
                         uint32_t v[NC][32];
+                        if (HS) {   // half h of the accumulator
+                            umma::mbar_wait(&S.accf[h], c & 1u);
+                            umma::fence_after();
+                        }
 #pragma unroll
                         for (int x = 0; x < NC; ++x) umma::tmem_ld32_nowait(tcol + 32 * (NC * h + x), v[x]);
                         umma::tmem_wait_ld();
-                        if (h == NL / NC - 1) {
+                        if (HS) {   // release this half at once
+                            umma::fence_before();
+                            __syncwarp();
+                            if (lane == 0) umma::mbar_arrive(&S.acce[h]);
+                            if (kProf && h == NL / NC - 1) { const long long t = clock64(); pr[1] += t - p1; p1 = t; }
+                        } else if (h == NL / NC - 1) {
                             umma::fence_before();
                             __syncwarp();
                             if (lane == 0) umma::mbar_arrive(&S.acce[ab]);
