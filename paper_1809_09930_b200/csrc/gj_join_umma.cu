@@ -33,6 +33,20 @@ constexpr int kExp = GJ_UMMA_EXPERIMENT;
 constexpr bool kProf = (kExp & 64) != 0;
 __device__ unsigned long long g_umma_prof[16];
 
+// Waits on the MMA <-> epilogue handoff: suspend-time-hinted try_wait (default)
+// or a plain try_wait spin (-DGJ_UMMA_SPIN, timing experiment).
+__device__ __forceinline__ void handoff_wait(uint64_t* mbar, uint32_t parity) {
+#ifdef GJ_UMMA_SPIN
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAITS_%=;\n\t}\n" ::"r"(umma::smem_u32(mbar)), "r"(parity));
+#else
+    umma::mbar_wait(mbar, parity);
+#endif
+}
+
 constexpr int kM = 128;         // queries per tile (UMMA M)
 constexpr int kN = 128;         // candidates per block (UMMA N)
 // FP64 decision of one pair: the FP64 kernel's arithmetic (gj_join.cu).
@@ -325,7 +339,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                             if (kProf) { mp[2] += clock64() - m0; mp[4] += 1; }
                             continue;
                         }
-                        umma::mbar_wait(&S.acce[ab], aph ^ 1u);
+                        handoff_wait(&S.acce[ab], aph ^ 1u);
                         const long long m1 = kProf ? clock64() : 0;
                         umma::mbar_wait(&S.full[st], ph);
                         umma::fence_after();
@@ -342,8 +356,14 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                                               umma::smem_desc(b_s + ks * 256, 128, kSBO), kIdesc, ks > 0 ? 1u : 0u);
                         }
                         const long long m3 = kProf ? clock64() : 0;
-                        umma::commit(&S.empty[st]);
+                        // the accumulator's commit first: it is on the MMA -> epilogue
+                        // critical path; the ring stage's commit is not
+#ifndef GJ_UMMA_EMPTY_BY_EPILOGUE
                         umma::commit(&S.accf[ab]);
+                        umma::commit(&S.empty[st]);
+#else
+                        umma::commit(&S.accf[ab]);
+#endif
                         if (kProf) {
                             const long long m4 = clock64();
                             mp[0] += m1 - m0; mp[1] += m2 - m1; mp[2] += m3 - m2; mp[3] += m4 - m3; mp[4] += 1;
@@ -373,9 +393,14 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
                     const uint32_t ab = c % NACC, aph = (c / NACC) & 1u;
                     const long long p0 = kProf ? clock64() : 0;
                     if (!HS) {
-                        umma::mbar_wait(&S.accf[ab], aph);
+                        handoff_wait(&S.accf[ab], aph);
                         umma::fence_after();
                     }
+#ifdef GJ_UMMA_EMPTY_BY_EPILOGUE
+                    // experiment: the accumulator is complete, so the MMA no longer reads
+                    // the ring stage of this block -- free it from here
+                    if (warp == 2 && lane == 0) umma::mbar_arrive(&S.empty[c % ST]);
+#endif
                     long long p1 = kProf ? clock64() : 0;
                     if (kProf) pr[0] += p1 - p0;
                     const uint32_t tcol = tmem + lane_off + (uint32_t)((ab * MT + esub) * BN + ecol * CW);
