@@ -74,13 +74,16 @@ __global__ void k_col_reduce(const double* __restrict__ X, int64_t m, int64_t rs
     }
 }
 
-// Sequential (deterministic) reduction of the block partials; one thread per column.
-__global__ void k_col_final(const double* __restrict__ part, const double* __restrict__ part2, int nb, int n,
-                            int mode, int64_t m, double* __restrict__ outa, double* __restrict__ outb) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+// Deterministic reduction of the block partials: one CTA per column, each
+// thread folds a fixed strided subset, then a fixed-shape tree (the result
+// does not depend on scheduling).
+__global__ void __launch_bounds__(256) k_col_final(const double* __restrict__ part, const double* __restrict__ part2,
+                                                  int nb, int n, int mode, int64_t m, double* __restrict__ outa,
+                                                  double* __restrict__ outb) {
+    __shared__ double sa[256], sb[256];
+    const int j = blockIdx.x, t = threadIdx.x;
     double a = mode == kMinMax ? INFINITY : 0.0, b = -INFINITY;
-    for (int i = 0; i < nb; ++i) {
+    for (int i = t; i < nb; i += 256) {
         if (mode == kMinMax) {
             a = fmin(a, part[(int64_t)i * n + j]);
             b = fmax(b, part2[(int64_t)i * n + j]);
@@ -88,6 +91,23 @@ __global__ void k_col_final(const double* __restrict__ part, const double* __res
             a += part[(int64_t)i * n + j];
         }
     }
+    sa[t] = a;
+    sb[t] = b;
+    __syncthreads();
+    for (int w = 128; w >= 1; w >>= 1) {
+        if (t < w) {
+            if (mode == kMinMax) {
+                sa[t] = fmin(sa[t], sa[t + w]);
+                sb[t] = fmax(sb[t], sb[t + w]);
+            } else {
+                sa[t] += sa[t + w];
+            }
+        }
+        __syncthreads();
+    }
+    if (t != 0) return;
+    a = sa[0];
+    b = sb[0];
     if (mode == kMinMax) {
         outa[j] = a;
         outb[j] = b;
@@ -185,6 +205,18 @@ __global__ void k_gather_points(const double* __restrict__ X, const uint32_t* __
     const double x = t < n ? X[(int64_t)idx[p] * n + ord[t]] : 0.0;
     pts[e] = x;
     if (pts32) pts32[e] = t < n ? __double2float_rn(x - mn[t]) : 0.0f;
+}
+
+// pts32[p][t] = fl32(pts[p][t] - min_t) (reordered dims), 0 in the padding columns.
+__global__ void k_make32(const double* __restrict__ pts, int64_t N, int n, int n_pad, const Meta* __restrict__ meta,
+                         float* __restrict__ pts32) {
+    __shared__ double mn[kMaxDim];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) mn[t] = meta->mins[meta->order[t]];
+    __syncthreads();
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * n_pad) return;
+    const int t = (int)(e % n_pad);
+    pts32[e] = t < n ? __double2float_rn(pts[e] - mn[t]) : 0.0f;
 }
 
 __global__ void k_heads(const uint64_t* __restrict__ key, int64_t N, uint32_t* __restrict__ head) {
@@ -404,7 +436,7 @@ int col_reduce(const double* X, int64_t m, int64_t rstride, int n, int mode, con
     double* part = nullptr;
     GJ_CUDA(pool_malloc(&part, 2 * (size_t)nb * n * sizeof(double), s));
     k_col_reduce<<<nb, bs, 2 * bs * sizeof(double), s>>>(X, m, rstride, n, mode, mean, part, part + (size_t)nb * n); count_launch();
-    k_col_final<<<(n + 127) / 128, 128, 0, s>>>(part, part + (size_t)nb * n, nb, n, mode, m, outa, outb); count_launch();
+    k_col_final<<<n, 256, 0, s>>>(part, part + (size_t)nb * n, nb, n, mode, m, outa, outb); count_launch();
     GJ_CUDA(cudaGetLastError());
     GJ_CUDA(cudaFreeAsync(part, s));
     return GJ_OK;
@@ -500,17 +532,26 @@ int tc_threshold_from(double eps, int n, int K, double S, double R2, double* thr
 }
 
 namespace {
-// pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond (one thread per element).
+// pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond: one thread per
+// (row, 8-column chunk), i.e. one 16-byte core-matrix row segment of the
+// grouped layout (g16), written with a single vector store.
 __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, int k16, double S,
                          const Meta* __restrict__ meta, __half* __restrict__ pts16) {
     __shared__ double mn[kMaxDim];
     for (int t = threadIdx.x; t < n; t += blockDim.x) mn[t] = meta->mins[meta->order[t]];
     __syncthreads();
+    const int nch = k16 / 8;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= N * k16) return;
-    const int64_t p = e / k16;
-    const int t = (int)(e - p * k16);
-    pts16[g16(p, t, k16)] = t < n ? __double2half(S * (pts[p * n_pad + t] - mn[t])) : __float2half(0.f);
+    if (e >= N * nch) return;
+    const int64_t p = e / nch;
+    const int c = (int)(e - p * nch);
+    union { uint4 u; __half h[8]; } v;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int t = 8 * c + i;
+        v.h[i] = t < n ? __double2half(S * (pts[p * n_pad + t] - mn[t])) : __float2half(0.f);
+    }
+    *reinterpret_cast<uint4*>(pts16 + g16(p, 8 * c, k16)) = v.u;
 }
 
 // norm16[p] = ||x^_p||^2 exactly (fp64), R2 = max over p, and the candidate-side
@@ -567,12 +608,16 @@ static int make_fp16(Index* ix, bool* ok) {
     // (<= 256 rows) that start at a row multiple of 8 never read past the allocation
     const size_t rows16 = (size_t)((N + 7) & ~7ll) + 256;
     GJ_CUDA(pool_malloc(&ix->pts16, rows16 * ix->k16 * sizeof(__half), s));
-    GJ_CUDA(cudaMemsetAsync(ix->pts16, 0, rows16 * ix->k16 * sizeof(__half), s));
+    {   // zero only the last (partial) 8-row group and the padding block: k_make16
+        // writes every element of the groups holding rows < N
+        const size_t z0 = (size_t)(N & ~7ll) * ix->k16;
+        GJ_CUDA(cudaMemsetAsync(ix->pts16 + z0, 0, (rows16 * ix->k16 - z0) * sizeof(__half), s));
+    }
     GJ_CUDA(pool_malloc(&ix->norm16, (size_t)N * sizeof(double), s));
     unsigned long long* d_r2 = nullptr;
     GJ_CUDA(pool_malloc(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
-    k_make16<<<blocks_for(N * ix->k16, 256), 256, 0, s>>>(ix->pts, N, n_mma, ix->n_pad, ix->k16, ix->tc_scale,
+    k_make16<<<blocks_for(N * (ix->k16 / 8), 256), 256, 0, s>>>(ix->pts, N, n_mma, ix->n_pad, ix->k16, ix->tc_scale,
                                                           ix->meta, ix->pts16); count_launch();
     k_norm16<<<blocks_for(N, 256), 256, 0, s>>>(N, n_mma, ix->k16, ix->pts16, ix->norm16, d_r2); count_launch();
     GJ_CUDA(cudaGetLastError());
@@ -648,8 +693,7 @@ int build_index(Index* ix, const double* X) {
     // 5. sorted, reordered point array
     GJ_CUDA(pool_malloc(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
     GJ_CUDA(pool_malloc(&ix->orig, N * sizeof(uint32_t), s));
-    if (want32) GJ_CUDA(pool_malloc(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
-    k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, ix->pts32); count_launch();
+    k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, nullptr); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     if (ix->filter >= 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
         bool tc_ok = false;
@@ -657,6 +701,11 @@ int build_index(Index* ix, const double* X) {
         if (!tc_ok) ix->filter = want32 ? 1 : 0;
     } else if (ix->filter == 1 && !want32) {
         ix->filter = 0;
+    }
+    if (ix->filter == 1) {   // the FP32 filter's operands fl32(x - min), only when it runs
+        GJ_CUDA(pool_malloc(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
+        k_make32<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(ix->pts, N, n, ix->n_pad, M, ix->pts32); count_launch();
+        GJ_CUDA(cudaGetLastError());
     }
     // 6. non-empty cells
     uint32_t *head = nullptr, *pos = nullptr, *d_tot = nullptr;
