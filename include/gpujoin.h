@@ -77,11 +77,15 @@ typedef struct {
                             filter 3, was removed: GJ_ERR_INVALID.)
                             gj_join_stats always runs the FP64 scan.                          */
     int32_t mma_tiles;   /* filter 2 only: queries per index tile, in units of 128:
-                            1 (or 0, default) = tiles of 128 queries, 2 = tiles of 256
-                            queries (each covered by two CTAs).  Every tcgen05 CTA holds one
-                            128-query A tile (UMMA M = 128), streams 128-candidate B blocks
-                            into two 128-column TMEM accumulator slots and runs two per
-                            SM.  The pair set does not depend on it.                         */
+                            1 (or 0, default) = tiles of 128 queries: one tcgen05 CTA per
+                            tile part holds one 128-query A tile (UMMA M = 128) and one
+                            128-column TMEM accumulator, streams 128-candidate B blocks, and
+                            runs four per SM (three for MMA depth 64..96; 256-candidate
+                            blocks, two per SM, beyond); 2 = tiles of 256 queries, two A
+                            tiles per CTA sharing every candidate block, one CTA per SM.
+                            (Environment GJ_UMMA_WS=1 selects the persistent kernel: one CTA
+                            per SM, four accumulator slots.)  The pair set does not depend
+                            on any of these.                                                  */
 } gj_options;
 
 /* Read-only description of a built index. */

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpujoin.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["gj_capi.cu", "gj_index.cu", "gj_join.cu", "gj_join32.cu", "gj_join_umma.cu", "gj_radix.cu"]
+SOURCES = ["gj_capi.cu", "gj_index.cu", "gj_join.cu", "gj_join32.cu", "gj_join_umma.cu", "gj_join_ws.cu", "gj_radix.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]

@@ -234,6 +234,8 @@ int launch_join32(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_
 // Tensor-core bound variants; kEmit / kCount only.
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);  // tcgen05 (gj_join_umma.cu)
 int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s);
+// Persistent tcgen05 join (gj_join_ws.cu): one CTA per SM, four accumulator slots.
+int launch_join_ws(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
 // Number of tile positions for (rank, world, batch, n_batches); sets first/step.
 void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
                  JoinArgs* a);

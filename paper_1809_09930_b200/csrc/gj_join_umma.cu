@@ -636,6 +636,14 @@ int launch_umma_kp(const Index* ix, const JoinParams& p, JoinMode mode, const Jo
 }  // namespace
 
 int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s) {
+    // GJ_UMMA_WS=1 selects the persistent kernel (gj_join_ws.cu; same pair set,
+    // measured at parity with this one on expo32 / expo16, 5 % faster at K = 80,
+    // 13 % slower on uniform16 -- DESIGN "Persistent tcgen05 join"); read once.
+    static const bool persistent = [] {
+        const char* e = getenv("GJ_UMMA_WS");
+        return e && atoi(e) != 0;
+    }();
+    if (persistent && ix->tile_q == kM) return launch_join_ws(ix, mode, a, s);
     const JoinParams p = join_params(ix);
     const bool sym = ix->opt.symmetric != 0;
     // A tiles per CTA = tile_q / 128.  MT = 1 (default): 128-candidate blocks,

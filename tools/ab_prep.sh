@@ -8,4 +8,4 @@ bits=${2:-0}
 rm -rf ab/$v && mkdir -p ab/$v
 cp -r paper_1809_09930_b200 include ab/$v/
 rm -rf ab/$v/paper_1809_09930_b200/build ab/$v/paper_1809_09930_b200/__pycache__ ab/$v/paper_1809_09930_b200/libgpujoin.so
-(cd ab/$v && GJ_NVCC_EXTRA="-DGJ_UMMA_EXPERIMENT=$bits" python -c "import sys; sys.path.insert(0,'.'); import importlib; print(importlib.import_module('paper_1809_09930_b200._build').build(force=True))")
+(cd ab/$v && GJ_NVCC_EXTRA="-DGJ_UMMA_EXPERIMENT=$bits ${GJ_NVCC_EXTRA:-}" python -c "import sys; sys.path.insert(0,'.'); import importlib; print(importlib.import_module('paper_1809_09930_b200._build').build(force=True))")
