@@ -188,6 +188,9 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* _
 // pts[p][t] = X[idx[p]][order[t]] (0 for t >= n); one thread per output element.
 // pts32 (optional): the same coordinate centred on the dimension minimum and
 // rounded to float32, fl32(x - min) -- input of the certified FP32 prefilter.
+// pts[p][t] = X[idx[p]][order[t]] (0 in the padding columns): one warp per
+// sorted row, lane t writes dims t, t + 32, ... (coalesced 256-byte rows, no
+// per-element 64-bit division).
 __global__ void k_gather_points(const double* __restrict__ X, const uint32_t* __restrict__ idx, int64_t N,
                                 int n, int n_pad, const Meta* __restrict__ meta, double* __restrict__ pts,
                                 float* __restrict__ pts32) {
@@ -198,13 +201,18 @@ __global__ void k_gather_points(const double* __restrict__ X, const uint32_t* __
         mn[t] = meta->mins[ord[t]];
     }
     __syncthreads();
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= N * n_pad) return;
-    int64_t p = e / n_pad;
-    int t = (int)(e - p * n_pad);
-    const double x = t < n ? X[(int64_t)idx[p] * n + ord[t]] : 0.0;
-    pts[e] = x;
-    if (pts32) pts32[e] = t < n ? __double2float_rn(x - mn[t]) : 0.0f;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = w0; p < N; p += nw) {
+        const double* src = X + (int64_t)idx[p] * n;
+        double* dst = pts + p * n_pad;
+        for (int t = lane; t < n_pad; t += 32) {
+            const double x = t < n ? src[ord[t]] : 0.0;
+            dst[t] = x;
+            if (pts32) pts32[p * n_pad + t] = t < n ? __double2float_rn(x - mn[t]) : 0.0f;
+        }
+    }
 }
 
 // pts32[p][t] = fl32(pts[p][t] - min_t) (reordered dims), 0 in the padding columns.
@@ -535,49 +543,51 @@ namespace {
 // pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n, 0 beyond: one thread per
 // (row, 8-column chunk), i.e. one 16-byte core-matrix row segment of the
 // grouped layout (g16), written with a single vector store.
-__global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, int k16, double S,
-                         const Meta* __restrict__ meta, __half* __restrict__ pts16) {
+// One thread per point: pts16[p][t] = fp16(S (pts[p][t] - min_t)) for t < n
+// (0 up to K - 4), norm16[p] = ||x^_p||^2 exactly in fp64 from the rounded
+// halves, the candidate-side augmented columns (1, 1, h_hi, h_lo) with
+// h = -||x^_p||^2 / 2, and R2 = max_p norm16[p].  Chunks of 8 halves go out as
+// 16-byte core-matrix rows (g16); the last chunk, which holds the augmented
+// columns, is written once the norm is known.
+template <int KP>
+__global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n_pad, double S,
+                         const Meta* __restrict__ meta, __half* __restrict__ pts16, double* __restrict__ norm16,
+                         unsigned long long* __restrict__ r2max) {
     __shared__ double mn[kMaxDim];
     for (int t = threadIdx.x; t < n; t += blockDim.x) mn[t] = meta->mins[meta->order[t]];
     __syncthreads();
-    const int nch = k16 / 8;
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= N * nch) return;
-    const int64_t p = e / nch;
-    const int c = (int)(e - p * nch);
-    union { uint4 u; __half h[8]; } v;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int t = 8 * c + i;
-        v.h[i] = t < n ? __double2half(S * (pts[p * n_pad + t] - mn[t])) : __float2half(0.f);
-    }
-    *reinterpret_cast<uint4*>(pts16 + g16(p, 8 * c, k16)) = v.u;
-}
-
-// norm16[p] = ||x^_p||^2 exactly (fp64), R2 = max over p, and the candidate-side
-// augmented columns (1, 1, h_hi, h_lo), h = -||x^_p||^2 / 2 (one thread per point).
-__global__ void k_norm16(int64_t N, int n, int k16, __half* __restrict__ pts16, double* __restrict__ norm16,
-                         unsigned long long* __restrict__ r2max) {
+    constexpr int NCH = KP / 8;
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double nrm = 0.0;
     if (p < N) {
-        for (int t = 0; t < n; ++t) {
-            const double hd = (double)__half2float(pts16[g16(p, t, k16)]);
-            nrm += hd * hd;
+        const double* row = pts + p * n_pad;
+        union { uint4 u; __half h[8]; } v;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int t = 8 * c + i;
+                v.h[i] = t < n ? __double2half(S * (row[t] - mn[t])) : __float2half(0.f);
+                const double hd = (double)__half2float(v.h[i]);
+                nrm += hd * hd;
+            }
+            if (c < NCH - 1) *reinterpret_cast<uint4*>(pts16 + g16(p, 8 * c, KP)) = v.u;
         }
-        norm16[p] = nrm;
         const double h = -0.5 * nrm;
         const __half hh = __double2half(h);
-        pts16[g16(p, k16 - 4, k16)] = __float2half(1.f);
-        pts16[g16(p, k16 - 3, k16)] = __float2half(1.f);
-        pts16[g16(p, k16 - 2, k16)] = hh;
-        pts16[g16(p, k16 - 1, k16)] = __double2half(h - (double)__half2float(hh));
+        v.h[4] = __float2half(1.f);
+        v.h[5] = __float2half(1.f);
+        v.h[6] = hh;
+        v.h[7] = __double2half(h - (double)__half2float(hh));
+        *reinterpret_cast<uint4*>(pts16 + g16(p, KP - 8, KP)) = v.u;
+        norm16[p] = nrm;
     }
     unsigned long long bits = (unsigned long long)__double_as_longlong(nrm);
 #pragma unroll
     for (int o = 16; o; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
     if ((threadIdx.x & 31) == 0) atomicMax(r2max, bits);
 }
+
 }  // namespace
 
 // Builds the fp16 operands; *ok = true if the tensor-core bound is certified.
@@ -617,9 +627,18 @@ static int make_fp16(Index* ix, bool* ok) {
     unsigned long long* d_r2 = nullptr;
     GJ_CUDA(pool_malloc(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
-    k_make16<<<blocks_for(N * (ix->k16 / 8), 256), 256, 0, s>>>(ix->pts, N, n_mma, ix->n_pad, ix->k16, ix->tc_scale,
-                                                          ix->meta, ix->pts16); count_launch();
-    k_norm16<<<blocks_for(N, 256), 256, 0, s>>>(N, n_mma, ix->k16, ix->pts16, ix->norm16, d_r2); count_launch();
+    switch (ix->k16) {
+#define GJ_MAKE16(KP)                                                                                            \
+    case KP:                                                                                                     \
+        k_make16<KP><<<blocks_for(N, 128), 128, 0, s>>>(ix->pts, N, n_mma, ix->n_pad, ix->tc_scale, ix->meta,   \
+                                                       ix->pts16, ix->norm16, d_r2);                             \
+        break;
+        GJ_MAKE16(16) GJ_MAKE16(32) GJ_MAKE16(48) GJ_MAKE16(64) GJ_MAKE16(80) GJ_MAKE16(96) GJ_MAKE16(112)
+        GJ_MAKE16(128)
+#undef GJ_MAKE16
+        default: set_error("fp16 operands: unsupported MMA depth"); return GJ_ERR_INVALID;
+    }
+    count_launch();
     GJ_CUDA(cudaGetLastError());
     unsigned long long h_r2 = 0;
     GJ_CUDA(cudaMemcpyAsync(&h_r2, d_r2, sizeof(h_r2), cudaMemcpyDeviceToHost, s));
@@ -693,7 +712,8 @@ int build_index(Index* ix, const double* X) {
     // 5. sorted, reordered point array
     GJ_CUDA(pool_malloc(&ix->pts, (size_t)N * ix->n_pad * sizeof(double), s));
     GJ_CUDA(pool_malloc(&ix->orig, N * sizeof(uint32_t), s));
-    k_gather_points<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M, ix->pts, nullptr); count_launch();
+    k_gather_points<<<(unsigned)std::min<int64_t>(blocks_for(N * 32, 256), 148 * 16), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M,
+                                                                                             ix->pts, nullptr); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     if (ix->filter >= 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
         bool tc_ok = false;

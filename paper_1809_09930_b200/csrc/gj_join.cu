@@ -407,7 +407,14 @@ static bool plan_parts(const Index* ix, const JoinArgs& a, std::vector<uint32_t>
         W += w;
         wmax = w > wmax ? w : wmax;
     }
-    const double target = W / (148.0 * 8.0);
+    // parts of about 1 / (148 x div) of the launch's work (div = 8; GJ_PLAN_DIV
+    // overrides it for timing experiments, read once)
+    static const double div = [] {
+        const char* e = getenv("GJ_PLAN_DIV");
+        const double v = e ? atof(e) : 0.0;
+        return v > 0.0 ? v : 8.0;
+    }();
+    const double target = W / (148.0 * div);
     if (!(target > 0.0) || wmax <= target) return false;
     off->resize((size_t)a.n_tiles + 1);
     uint64_t acc = 0;

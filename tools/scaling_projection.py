@@ -22,13 +22,14 @@ p = argparse.ArgumentParser()
 p.add_argument("--workload", default="expo32")
 p.add_argument("--reps", type=int, default=5)
 p.add_argument("--bus-gbs", type=float, default=725.0, help="NVLink bus bandwidth for the broadcast model")
+p.add_argument("--worlds", default="1,2,4,8")
 a = p.parse_args()
 w = synth.WORKLOADS[a.workload]
 D = torch.from_numpy(synth.make(w["gen"], w["count"], w["dims"], seed=0)).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 batch_streams = [torch.cuda.Stream() for _ in range(3)]   # as bench.py: three batch streams
 res = {}
-for world in (1, 2, 4, 8):
+for world in [int(x) for x in a.worlds.split(",")]:
     per_rank = []
     for rank in range(world):
         runs = []
