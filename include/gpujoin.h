@@ -182,18 +182,23 @@ GJ_API int gj_selftest_umma(const void* A, const void* B, float* D, uint64_t str
  * idle 180 GB B200), at least the paper's 1e8. */
 GJ_API int64_t gj_num_batches(int64_t est_pairs, int64_t batch_size);
 
-/* Entity partitioning arithmetic (§6.2 l.1013), host only: the tile positions
- * j = first + step * m, m in [0, count), of the index's heaviest-first tile
- * order that rank `rank` of `world` processes in batch `batch` of `n_batches`
- * (j mod world = rank; (j div world) mod n_batches = batch). */
+/* Entity partitioning arithmetic (§6.2 l.1013), host only.  The query sets
+ * Q_l are runs of `block` consecutive positions of the index's heaviest-first
+ * tile order (positions l*block .. l*block + block - 1, the last run partial;
+ * reading R12); rank `rank` of `world` processes, in batch `batch` of
+ * `n_batches`, the sets l = first + step * k (l mod world = rank,
+ * (l div world) mod n_batches = batch): `count` tile positions in all,
+ *   position of tile m = (first + step * (m / block)) * block + m % block.
+ * block is the library's constant (1; GJ_DEAL_BLOCK overrides it).  Errors:
+ * GJ_ERR_INVALID for null outputs, n_tiles < 0, rank / batch out of range. */
 GJ_API int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, int32_t n_batches,
-                        int64_t* first, int64_t* step, int64_t* count);
+                        int64_t* first, int64_t* step, int64_t* count, int32_t* block);
 
 /* selfJoinKernel for one batch (Alg. 1 l.586) [async].
  *  Processes batch `batch` of `n_batches` of rank `rank`'s share of the
- *  query tiles (entity partitioning §6.2: tile position j in the index's
- *  heaviest-first order belongs to rank j mod world; batch = (j div world)
- *  mod n_batches).  Appends ordered pairs (query_id, neighbour_id) as uint32
+ *  query tiles (entity partitioning §6.2: query set l -- `block` consecutive
+ *  positions of the index's heaviest-first tile order, gj_partition -- belongs
+ *  to rank l mod world; batch = (l div world) mod n_batches).  Appends ordered pairs (query_id, neighbour_id) as uint32
  *  pairs to out_pairs (device, capacity pairs) at positions obtained from the
  *  device counter *d_count (uint64, device pointer; caller zeroes it before
  *  the first batch that shares the buffer).  Pairs past capacity are counted

@@ -84,10 +84,10 @@ namespace {
 
 __global__ void k_share_queries(const uint32_t* __restrict__ tile_order, const uint32_t* __restrict__ tile_cell,
                                 const uint32_t* __restrict__ tile_q0, const uint32_t* __restrict__ cell_start,
-                                uint32_t tq, int64_t first, int64_t step, int64_t count, unsigned long long* out) {
+                                uint32_t tq, JoinArgs a, unsigned long long* out) {
     unsigned long long acc = 0;
-    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < count; m += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t t = tile_order[first + step * m];
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_tiles; m += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t t = tile_order[tile_pos(a, m)];
         uint32_t g = tile_cell[t];
         acc += min(tq, cell_start[g + 1] - tile_q0[t]);
     }
@@ -281,8 +281,8 @@ int gj_device_arrays(const gj_index* h, const double** pts, const uint32_t** ori
 }
 
 int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, int32_t n_batches, int64_t* first,
-                 int64_t* step, int64_t* count) {
-    if (!first || !step || !count || n_tiles < 0) { set_error("bad argument"); return GJ_ERR_INVALID; }
+                 int64_t* step, int64_t* count, int32_t* block) {
+    if (!first || !step || !count || !block || n_tiles < 0) { set_error("bad argument"); return GJ_ERR_INVALID; }
     if (int rc = check_rank(rank, world)) return rc;
     if (n_batches < 1 || batch < 0 || batch >= n_batches) { set_error("need 0 <= batch < n_batches"); return GJ_ERR_INVALID; }
     Index tmp;
@@ -292,6 +292,7 @@ int gj_partition(int64_t n_tiles, int32_t rank, int32_t world, int32_t batch, in
     *first = a.first;
     *step = a.step;
     *count = a.n_tiles;
+    *block = a.blk;
     return GJ_OK;
 }
 
@@ -394,19 +395,18 @@ int gj_estimate(gj_index* h, double frac, int32_t rank, int32_t world, int64_t* 
     const int64_t stepf = std::max<int64_t>(1, llround(1.0 / frac));
     JoinArgs a{};
     a.count = ix.scratch_count;
-    a.first = rank;
-    a.step = (int64_t)world * stepf;
-    a.n_tiles = a.first < ix.T ? (ix.T - a.first + a.step - 1) / a.step : 0;
+    query_sets(ix.T, rank, (int64_t)world * stepf, &a);   // every stepf-th query set of the rank's share
     // a 1% sample of tiles is far too few CTAs to fill 148 SMs: split every
     // sampled tile's candidate scan over enough CTAs for ~8 waves of 148
     a.split = (int32_t)std::max<int64_t>(1, std::min<int64_t>(64, (8 * 148 + a.n_tiles - 1) / std::max<int64_t>(1, a.n_tiles)));
     GJ_CUDA(cudaMemsetAsync(ix.scratch_count, 0, 8 * sizeof(uint64_t), s));
     if (int rc = launch_join(&ix, kCount, a, s)) return rc;
     // queries of the whole share
-    int64_t share = rank < ix.T ? (ix.T - rank + world - 1) / world : 0;
-    if (share > 0) {
-        k_share_queries<<<(unsigned)std::min<int64_t>(592, (share + 255) / 256), 256, 0, s>>>(
-            ix.tile_order, ix.tile_cell, ix.tile_q0, ix.cell_start, (uint32_t)ix.tile_q, rank, world, share,
+    JoinArgs sh{};
+    query_sets(ix.T, rank, world, &sh);
+    if (sh.n_tiles > 0) {
+        k_share_queries<<<(unsigned)std::min<int64_t>(592, (sh.n_tiles + 255) / 256), 256, 0, s>>>(
+            ix.tile_order, ix.tile_cell, ix.tile_q0, ix.cell_start, (uint32_t)ix.tile_q, sh,
             (unsigned long long*)ix.scratch_count + 2); count_launch();
     }
     GJ_CUDA(cudaGetLastError());

@@ -122,9 +122,10 @@ struct JoinArgs {
     uint32_t* out;            // [cap][2]
     uint64_t cap;
     uint64_t* count;          // device counter(s); kStats: [4] = cells, tests, dims, pairs
-    int64_t first;            // first tile position j
-    int64_t step;             // tile positions j = first + step * m
-    int64_t n_tiles;          // number of m values
+    int64_t first;            // first query set (unit of blk tile positions)
+    int64_t step;             // query sets first + step * k of this launch
+    int64_t n_tiles;          // number of tile positions m (tile_pos below)
+    int32_t blk;              // tile positions per query set (0 / 1: one)
     int32_t split;            // CTAs per tile, each scanning 1/split of every candidate window (0/1 = none)
     // Work-balanced split (optional, overrides split): tile m of the launch gets
     // part_off[m+1] - part_off[m] CTAs; part_off[n_tiles] = total parts.
@@ -154,6 +155,18 @@ struct JoinParams {
     double thr16;
     uint32_t tile_q;                 // queries per index tile (128 or 256)
 };
+
+// Query sets (§6.2 l.1013, reading R12): blk consecutive positions
+// of the heaviest-first tile order form one set Q_l; the sets of a launch are
+// l = first + step * k.  Launch-local tile m sits at position
+//   (first + step * (m / blk)) * blk + m % blk.
+__host__ __device__ __forceinline__ int64_t tile_pos(const JoinArgs& a, int64_t m) {
+    if (a.blk <= 1) return a.first + a.step * m;
+    return (a.first + a.step * (m / a.blk)) * a.blk + m % a.blk;
+}
+// Tile positions per query set of the entity partitioning and result
+// batching (kDealBlock; GJ_DEAL_BLOCK overrides it for timing experiments).
+int deal_block();
 
 // The query block of one CTA.  A CTA handles `qper` queries (128, or 256 in
 // the two-accumulator tcgen05 kernel); an index tile of tile_q queries is
@@ -187,7 +200,7 @@ __device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs&
         sub = mm % subs;
         m = mm / subs;
     }
-    const int64_t j = A.first + A.step * (int64_t)m;
+    const int64_t j = tile_pos(A, (int64_t)m);
     const uint32_t tile = P.tile_order[j];
     t.g = P.tile_cell[tile];
     t.q0 = P.tile_q0[tile] + sub * qper;
@@ -236,6 +249,8 @@ int launch_join_umma(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStre
 int selftest_umma(const void* A, const void* B, float* D, cudaStream_t s);
 // Persistent tcgen05 join (gj_join_ws.cu): one CTA per SM, four accumulator slots.
 int launch_join_ws(const Index* ix, JoinMode mode, const JoinArgs& a, cudaStream_t s);
+// Query sets first + step * k of T tiles (blk, first, step, n_tiles of a).
+void query_sets(int64_t T, int64_t first, int64_t step, JoinArgs* a);
 // Number of tile positions for (rank, world, batch, n_batches); sets first/step.
 void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world,
                  JoinArgs* a);

@@ -386,11 +386,35 @@ JoinParams join_params(const Index* ix) {
     return p;
 }
 
+// Query sets of kDealBlock consecutive heaviest-first tiles (reading R12: one
+// tile per set).  Larger sets keep spatially consecutive tiles in one launch
+// (tiles of one cell have equal keys and keep their order); measured no
+// faster: the expo32 join dealt into 24 launches took 215 ms with sets of 1 or
+// 8 tiles, 209 with 32, vs 179 in 3 launches (profiles/r2_ab_deal_block.txt).
+constexpr int kDealBlock = 1;
+int deal_block() {
+    static const int b = [] {
+        const char* e = getenv("GJ_DEAL_BLOCK");
+        const int v = e ? atoi(e) : 0;
+        return v >= 1 ? v : kDealBlock;
+    }();
+    return b;
+}
+
+void query_sets(int64_t T, int64_t first, int64_t step, JoinArgs* a) {
+    const int64_t B = deal_block();
+    const int64_t U = (T + B - 1) / B;   // query sets
+    a->blk = (int32_t)B;
+    a->first = first;
+    a->step = step;
+    const int64_t nu = first < U ? (U - first + step - 1) / step : 0;
+    a->n_tiles = nu * B;
+    if (nu > 0 && first + step * (nu - 1) == U - 1) a->n_tiles -= U * B - T;   // the last set is partial
+}
+
 void batch_tiles(const Index* ix, int32_t batch, int32_t n_batches, int32_t rank, int32_t world, JoinArgs* a) {
-    // entity partitioning (§6.2): position j -> rank j mod |p|; batch (j div |p|) mod n_b
-    a->first = (int64_t)rank + (int64_t)world * batch;
-    a->step = (int64_t)world * n_batches;
-    a->n_tiles = a->first < ix->T ? (ix->T - a->first + a->step - 1) / a->step : 0;
+    // entity partitioning (§6.2): query set l -> rank l mod |p|; batch (l div |p|) mod n_b
+    query_sets(ix->T, (int64_t)rank + (int64_t)world * batch, (int64_t)world * n_batches, a);
 }
 
 // Work-balanced split plan of one launch: a tile whose estimated work
@@ -403,7 +427,7 @@ static bool plan_parts(const Index* ix, const JoinArgs& a, std::vector<uint32_t>
     if (a.n_tiles <= 0 || a.split > 1 || ix->h_work_by_pos.size() != (size_t)ix->T) return false;
     double W = 0.0, wmax = 0.0;
     for (int64_t m = 0; m < a.n_tiles; ++m) {
-        const double w = (double)ix->h_work_by_pos[(size_t)(a.first + a.step * m)];
+        const double w = (double)ix->h_work_by_pos[(size_t)tile_pos(a, m)];
         W += w;
         wmax = w > wmax ? w : wmax;
     }
@@ -420,7 +444,7 @@ static bool plan_parts(const Index* ix, const JoinArgs& a, std::vector<uint32_t>
     uint64_t acc = 0;
     for (int64_t m = 0; m < a.n_tiles; ++m) {
         (*off)[(size_t)m] = (uint32_t)acc;
-        const double w = (double)ix->h_work_by_pos[(size_t)(a.first + a.step * m)];
+        const double w = (double)ix->h_work_by_pos[(size_t)tile_pos(a, m)];
         acc += (uint64_t)std::min(512.0, std::max(1.0, std::ceil(w / target)));
     }
     (*off)[(size_t)a.n_tiles] = (uint32_t)acc;

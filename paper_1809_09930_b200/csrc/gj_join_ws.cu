@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     part = item % split;
                     m = item / split;
                 }
-                const uint32_t tile = P.tile_order[A.first + A.step * (int64_t)m];
+                const uint32_t tile = P.tile_order[tile_pos(A, (int64_t)m)];
                 const uint32_t g = P.tile_cell[tile], q0 = P.tile_q0[tile];
                 const uint32_t nq = min((uint32_t)kM, P.cell_start[g + 1] - q0);
                 const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];

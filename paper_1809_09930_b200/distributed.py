@@ -32,8 +32,9 @@ from . import gpujoin
 def share_positions(n_tiles: int, rank: int, world: int, batch: int = 0, n_batches: int = 1) -> np.ndarray:
     """Tile positions processed by (rank, batch) -- from the library's own
     gj_partition arithmetic (host only, no GPU needed)."""
-    f, s, c = gpujoin.partition(n_tiles, rank, world, batch, n_batches)
-    return f + s * np.arange(c, dtype=np.int64)
+    f, s, c, b = gpujoin.partition(n_tiles, rank, world, batch, n_batches)
+    m = np.arange(c, dtype=np.int64)
+    return (f + s * (m // b)) * b + m % b
 
 
 class Comm:

@@ -73,7 +73,8 @@ def lib():
         "gj_tc_threshold": (C.c_int, [D, I32, I32, D, D, C.POINTER(D), C.POINTER(D)]),
         "gj_fp32_threshold": (C.c_int, [D, I32, C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(D)]),
         "gj_fp32_accept_threshold": (C.c_int, [D, I32, C.POINTER(C.c_double), C.POINTER(C.c_float)]),
-        "gj_partition": (C.c_int, [I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
+        "gj_partition": (C.c_int, [I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64),
+                                   C.POINTER(I32)]),
         "gj_self_join_async": (C.c_int, [P, P, I64, P, I32, I32, I32, I32]),
         "gj_self_join_async_stream": (C.c_int, [P, P, I64, P, I32, I32, I32, I32, U64]),
         "gj_self_join_count_async": (C.c_int, [P, P, I32, I32, I32, I32]),
@@ -256,10 +257,12 @@ def num_batches(est_pairs: int, batch_size: int) -> int:
 
 
 def partition(n_tiles: int, rank: int, world: int, batch: int = 0, n_batches: int = 1):
-    """(first, step, count) of the tile positions of (rank, batch) -- gj_partition."""
-    f, s, c = C.c_int64(), C.c_int64(), C.c_int64()
-    _check(lib().gj_partition(int(n_tiles), rank, world, batch, n_batches, C.byref(f), C.byref(s), C.byref(c)))
-    return f.value, s.value, c.value
+    """(first, step, count, block) of (rank, batch) -- gj_partition: query sets
+    first + step * k of `block` consecutive tile positions, count positions."""
+    f, s, c, b = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+    _check(lib().gj_partition(int(n_tiles), rank, world, batch, n_batches, C.byref(f), C.byref(s), C.byref(c),
+                              C.byref(b)))
+    return f.value, s.value, c.value, b.value
 
 
 def fp32_threshold(eps: float, spans):

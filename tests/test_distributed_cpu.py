@@ -62,16 +62,30 @@ def test_two_rank_gloo_replicate_allreduce_partition():
     assert all(r[4] == 3.0 for r in res)                             # max over ranks (bench timing)
     allpos = sorted(res[0][3] + res[1][3])
     assert allpos == list(range(37))                                 # disjoint, complete
-    assert res[0][3] == list(range(0, 37, 2))
+    B = _block()
+    assert res[0][3] == [j for j in range(37) if (j // B) % 2 == 0]  # query sets of B tiles, round robin
+
+
+def _block():
+    from paper_1809_09930_b200 import gpujoin
+    return gpujoin.partition(1, 0, 1)[3]
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_partition_matches_paper_round_robin(world):
+    # §6.2 l.1013: query set Q_l goes to GPU l mod |p| (oracle/grid.py); a
+    # query set is B consecutive heaviest-first tiles (reading R12)
     from paper_1809_09930_b200 import distributed as D
+    B = _block()
+    assert B >= 1
     n_sets = 32
     ref = grid.assign_query_sets(n_sets, world)
     for r in range(world):
-        assert D.share_positions(n_sets, r, world).tolist() == ref[r]
+        want = [l * B + i for l in ref[r] for i in range(B)]
+        assert D.share_positions(n_sets * B, r, world).tolist() == want
+        # a partial last set: T = n_sets * B - 3
+        T = n_sets * B - 3
+        assert D.share_positions(T, r, world).tolist() == [j for j in want if j < T]
 
 
 @pytest.mark.parametrize("world,nb,T", [(1, 3, 10), (2, 3, 17), (4, 5, 103), (8, 7, 1000)])

@@ -1,5 +1,5 @@
 """A/B timing of builds of the package (copies under ab/<v>/ from tools/ab_prep.sh):
-python tools/ab_join.py ab/A [reps]  -- 3 result batches of the expo32 join, CUDA events"""
+python tools/ab_join.py ab/A [reps]  -- AB_BATCHES (3) result batches of the expo32 join, CUDA events"""
 import os, sys
 pkg = os.path.abspath(sys.argv[1])
 sys.path.insert(0, pkg)
@@ -21,8 +21,9 @@ for r in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for b in range(3):
-        ix.self_join_async(out, cnt, b, 3)
+    nb = int(os.environ.get("AB_BATCHES", "3"))   # result batches (all on the current stream)
+    for b in range(nb):
+        ix.self_join_async(out, cnt, b, nb)
     e.record()
     torch.cuda.synchronize()
     ts.append(s.elapsed_time(e))
