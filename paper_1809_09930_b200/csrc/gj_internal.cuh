@@ -177,13 +177,13 @@ struct CtaTile {
     uint32_t g, q0, nq;
     int part, split;
 };
-__device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs& A, uint32_t qper) {
+__device__ __forceinline__ CtaTile cta_tile_at(const JoinParams& P, const JoinArgs& A, uint32_t qper, uint32_t b) {
     const uint32_t subs = P.tile_q > qper ? P.tile_q / qper : 1u;
     CtaTile t;
     uint32_t m, sub;
-    if (A.part_off) {   // CTA b: (unit r = b / subs, sub = b % subs), unit r -> (tile m, part)
-        sub = blockIdx.x % subs;
-        const uint32_t r = blockIdx.x / subs;
+    if (A.part_off) {   // item b: (unit r = b / subs, sub = b % subs), unit r -> (tile m, part)
+        sub = b % subs;
+        const uint32_t r = b / subs;
         uint32_t lo = 0, hi = (uint32_t)A.n_tiles;   // last m with part_off[m] <= r
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
@@ -194,9 +194,9 @@ __device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs&
         t.split = (int)(A.part_off[m + 1] - A.part_off[m]);
     } else {
         const uint32_t split = A.split > 1 ? (uint32_t)A.split : 1u;
-        t.part = (int)(blockIdx.x % split);
+        t.part = (int)(b % split);
         t.split = (int)split;
-        const uint32_t mm = blockIdx.x / split;
+        const uint32_t mm = b / split;
         sub = mm % subs;
         m = mm / subs;
     }
@@ -207,6 +207,9 @@ __device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs&
     const uint32_t end = P.cell_start[t.g + 1];
     t.nq = t.q0 < end ? min(qper, end - t.q0) : 0u;
     return t;
+}
+__device__ __forceinline__ CtaTile cta_tile(const JoinParams& P, const JoinArgs& A, uint32_t qper) {
+    return cta_tile_at(P, A, qper, blockIdx.x);
 }
 // CTAs of a launch over a.n_tiles index tiles with `qper` queries per CTA.
 inline unsigned grid_ctas(const JoinArgs& a, int tile_q, int qper) {

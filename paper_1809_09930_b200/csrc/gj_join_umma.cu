@@ -137,7 +137,7 @@ struct WsSmem {
     alignas(128) __half a[MT][kM * KP];                           // queries (A), canonical K-major layout
     alignas(128) __half b[ws_stages<KP, BN, MT, SL>()][BN * KP];   // candidate ring (B)
     uint64_t full[ws_stages<KP, BN, MT, SL>()], empty[ws_stages<KP, BN, MT, SL>()], accf[2 * SL], acce[2 * SL];
-    uint32_t tmem_base;
+    uint32_t tmem_base, item;
     uint32_t wr[kMaxWin], ws[kMaxWin], nbk[kMaxWin];          // window [r, s), blocks (bit 31: own cell)
     uint2 sv[4 * MT * EPW][64];                               // per epilogue warp: staged survivors (qpos, cpos)
     unsigned long long red[ws_warps<MT, EPW>()];
@@ -160,7 +160,7 @@ struct WsSmem {
 //               cell) for a lane-parallel FP64 decision.
 template <int KP, int BN, int MT, int SL, int EPW, int MODE, bool SYM>
 __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, BN, MT, SL>())
-    k_join_umma(JoinParams P, JoinArgs A) {
+    k_join_umma(JoinParams P, JoinArgs A, uint32_t* __restrict__ work_counter, uint32_t n_items) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WsSmem<KP, BN, MT, SL, EPW>& S = *reinterpret_cast<WsSmem<KP, BN, MT, SL, EPW>*>(smem_raw);
     constexpr int NE = 4 * MT * EPW;       // epilogue warps
@@ -194,12 +194,15 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
     constexpr int NBAR = HS ? 2 : NACC;
     constexpr uint32_t kIdescH = umma::idesc_f16_f32(kM, BN / 2);
 
-    const CtaTile ct = cta_tile(P, A, QT);
-    if (ct.nq == 0) return;   // sub-block past the end of the tile's cell
+    // One A tile per CTA (MT = 1): persistent CTAs pull (tile, part) items
+    // from an atomic counter (TMEM, barriers and the block pipeline set up
+    // once; the last items are the lightest, so no static tail).  MT = 2: one
+    // item per CTA (the release count depends on the item's A tiles).
+    constexpr bool kPersist = MT == 1;
+    CtaTile ct = cta_tile(P, A, QT);
+    if (!kPersist && ct.nq == 0) return;   // sub-block past the end of the tile's cell
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int part = ct.part, split = ct.split;
-    const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
-    const int nsub = (int)((nq + kM - 1) / kM);   // A tiles holding queries (1..MT)
+    const int nsub = kPersist ? 1 : (int)((ct.nq + kM - 1) / kM);   // A tiles holding queries (1..MT)
     const int n_pad = P.n_pad;
     const double eps = P.eps;
 
@@ -215,6 +218,21 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
         }
         umma::mbar_fence_init();
     }
+    unsigned long long npairs = 0, queries = 0;
+    uint32_t cnt = 0;   // blocks consumed so far (identical sequence in every role, across items)
+    for (;;) {   // ------------------------------------------------------- items
+    if (kPersist) {
+        __syncthreads();   // everyone has read the previous item
+        if (tid == 0) S.item = atomicAdd(work_counter, 1u);
+        __syncthreads();
+        const uint32_t item = S.item;
+        if (item >= n_items) break;
+        ct = cta_tile_at(P, A, QT, item);
+        if (ct.nq == 0) continue;
+    }
+    const int part = ct.part, split = ct.split;
+    const uint32_t g = ct.g, q0 = ct.q0, nq = ct.nq;
+    if (tid == 0 && part == 0) queries += nq;
     for (int row = tid - 64; row >= 0 && row < QT; row += 32 * NE) {   // A tiles: thread = query row
         const int sub = row >> 7, rr = row & (kM - 1);
         const bool valid = row < (int)nq;
@@ -230,7 +248,6 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
             *reinterpret_cast<uint4*>(a_raw + umma::tile_off(rr, kc * 8, KP)) = c.u;
         }
     }
-    unsigned long long npairs = 0;
     if (SYM && part == 0 && tid < QT) {   // the self pair (q, q)
         const bool active = tid < (int)nq;
         const uint32_t qid = P.orig[q0 + (active ? tid : 0)];
@@ -256,7 +273,6 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
     const double u_lo = P.pts[(size_t)q0 * n_pad + P.u];
     const double u_hi = P.pts[(size_t)(q0 + nq - 1) * n_pad + P.u];
     const uint32_t nb0 = SYM ? P.nbr_self[g] : P.nbr_off[g], nb1 = P.nbr_off[g + 1];
-    uint32_t cnt = 0;   // blocks consumed so far (identical sequence in every role)
     const int eidx = (warp - 2) >> 2;               // epilogue: (A tile, column part) of this warp
     const int esub = eidx % MT, ecol = eidx / MT;
     const int erow = kM * esub + 32 * (warp & 3) + lane;   // query row; TMEM lane = erow % 128
@@ -510,9 +526,11 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
         for (int i = 0; i < nwin; ++i) cnt += S.nbk[i] & 0x7fffffffu;
         __syncthreads();
     }
+    if (!kPersist) break;
+    }   // items
     umma::fence_before();
     __syncthreads();
-    if (warp == 1) umma::tmem_dealloc(tmem, TCOLS);
+    if (warp == 1) umma::tmem_dealloc(S.tmem_base, TCOLS);
     // executed accumulator entries (rows x columns of every block, padding included)
     if (A.mma_tests && tid == 0 && cnt) atomicAdd(A.mma_tests, (unsigned long long)cnt * (kM * nsub) * BN);
 
@@ -526,7 +544,7 @@ __global__ void __launch_bounds__(32 * ws_warps<MT, EPW>(), ws_ctas_per_sm<KP, B
             unsigned long long t = 0;
             for (int w = 0; w < NW; ++w) t += S.red[w];
             if (t) atomicAdd((unsigned long long*)A.count, t);
-            if (part == 0) atomicAdd((unsigned long long*)A.count + 1, (unsigned long long)nq);
+            if (queries) atomicAdd((unsigned long long*)A.count + 1, queries);
         }
     }
 }
@@ -598,10 +616,21 @@ int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_done.fetch_or(bit);
     }
-    k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM>
-        <<<grid_ctas(a, (int)p.tile_q, kM * MT), 32 * ws_warps<MT, EPW>(), smem, s>>>(p, a);
+    const unsigned total = grid_ctas(a, (int)p.tile_q, kM * MT);
+    if (total == 0) return GJ_OK;
+    uint32_t* counter = nullptr;
+    unsigned grid = total;
+    if (MT == 1) {   // persistent CTAs: as many as fit, items from an atomic counter
+        static int n_sm = 0;
+        if (!n_sm) GJ_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        grid = std::min<unsigned>(total, (unsigned)(n_sm * kCtas));
+        GJ_CUDA(pool_malloc(&counter, sizeof(uint32_t), s));
+        GJ_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
+    }
+    k_join_umma<KP, BN, MT, SL, EPW, MODE, SYM><<<grid, 32 * ws_warps<MT, EPW>(), smem, s>>>(p, a, counter, total);
     count_launch();
     GJ_CUDA(cudaGetLastError());
+    if (counter) GJ_CUDA(cudaFreeAsync(counter, s));
     return GJ_OK;
 }
 
