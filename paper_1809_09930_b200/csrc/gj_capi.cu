@@ -397,14 +397,17 @@ int gj_estimate(gj_index* h, double frac, int32_t rank, int32_t world, int64_t* 
     a.count = ix.scratch_count;
     query_sets(ix.T, rank, (int64_t)world * stepf, &a);   // every stepf-th query set of the rank's share
     // a 1% sample of tiles is too few CTAs to fill 148 SMs when its tiles are
-    // heavy: the work-balanced plan of launch_join splits the heavy sampled
-    // tiles (GJ_EST_UNIFORM=1: the round-1 uniform split of every sampled tile
-    // over ~8 waves of 148 CTAs, which repeats the window set-up of light tiles)
-    static const bool uniform = [] {
+    // heavy.  Fewer sampled tiles than SMs (a rank's share on several GPUs):
+    // every sampled tile's candidate scan is split over ~8 waves of 148 CTAs;
+    // otherwise the work-balanced plan of launch_join splits only the heavy
+    // ones (a uniform split repeats the window set-up of light tiles: songs90
+    // estimate 2.8 -> 0.4 ms, profiles/r2_ab_estimator_split.txt).
+    // GJ_EST_UNIFORM=0 / 1 forces either.
+    static const int force = [] {
         const char* e = getenv("GJ_EST_UNIFORM");
-        return e && atoi(e) != 0;
+        return e ? atoi(e) : -1;
     }();
-    if (uniform)
+    if (force == 1 || (force < 0 && a.n_tiles < 148))
         a.split = (int32_t)std::max<int64_t>(1, std::min<int64_t>(64, (8 * 148 + a.n_tiles - 1) / std::max<int64_t>(1, a.n_tiles)));
     GJ_CUDA(cudaMemsetAsync(ix.scratch_count, 0, 8 * sizeof(uint64_t), s));
     if (int rc = launch_join(&ix, kCount, a, s)) return rc;

@@ -23,6 +23,7 @@
 #include <cmath>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "gj_internal.cuh"
@@ -591,7 +592,7 @@ __global__ void k_make16(const double* __restrict__ pts, int64_t N, int n, int n
 }  // namespace
 
 // Builds the fp16 operands; *ok = true if the tensor-core bound is certified.
-static int make_fp16(Index* ix, bool* ok) {
+static int make_fp16(Index* ix, unsigned long long* d_r2, bool* ok) {
     cudaStream_t s = ix->stream;
     const Meta& m = ix->h_meta;
     // dims carried by the MMA: the first n_mma of the REORDER order (all n by
@@ -624,8 +625,6 @@ static int make_fp16(Index* ix, bool* ok) {
         GJ_CUDA(cudaMemsetAsync(ix->pts16 + z0, 0, (rows16 * ix->k16 - z0) * sizeof(__half), s));
     }
     GJ_CUDA(pool_malloc(&ix->norm16, (size_t)N * sizeof(double), s));
-    unsigned long long* d_r2 = nullptr;
-    GJ_CUDA(pool_malloc(&d_r2, sizeof(*d_r2), s));
     GJ_CUDA(cudaMemsetAsync(d_r2, 0, sizeof(*d_r2), s));
     switch (ix->k16) {
 #define GJ_MAKE16(KP)                                                                                            \
@@ -640,13 +639,17 @@ static int make_fp16(Index* ix, bool* ok) {
     }
     count_launch();
     GJ_CUDA(cudaGetLastError());
-    unsigned long long h_r2 = 0;
-    GJ_CUDA(cudaMemcpyAsync(&h_r2, d_r2, sizeof(h_r2), cudaMemcpyDeviceToHost, s));
-    GJ_CUDA(cudaFreeAsync(d_r2, s));
-    GJ_CUDA(cudaStreamSynchronize(s));
+    *ok = true;   // launched; make_fp16_finish decides once R2 is on the host
+    return GJ_OK;
+}
+
+// The certified threshold from R2 = max ||x^||^2 (read back by the caller
+// together with its next count); frees the operands when it is not useful.
+static int make_fp16_finish(Index* ix, unsigned long long h_r2, bool* ok) {
+    cudaStream_t s = ix->stream;
     double R2;
     memcpy(&R2, &h_r2, sizeof(R2));
-    *ok = tc_threshold_from(ix->eps, n_mma, ix->k16, ix->tc_scale, R2, &ix->thr16, &ix->margin16) != 0;
+    *ok = tc_threshold_from(ix->eps, ix->n_mma, ix->k16, ix->tc_scale, R2, &ix->thr16, &ix->margin16) != 0;
     if (!*ok) {
         GJ_CUDA(cudaFreeAsync(ix->pts16, s));
         GJ_CUDA(cudaFreeAsync(ix->norm16, s));
@@ -656,6 +659,36 @@ static int make_fp16(Index* ix, bool* ok) {
     return GJ_OK;
 }
 
+
+// Small pinned host blocks for the build's read-backs (a pageable
+// cudaMemcpyAsync device -> host waits for the stream, i.e. is one more
+// synchronisation), reused across builds and threads.
+namespace {
+struct Staging {
+    Meta meta;
+    unsigned long long r2;
+    uint32_t count;
+};
+std::mutex g_stage_mu;
+std::vector<Staging*> g_stage_free;
+struct StagingLease {
+    Staging* p = nullptr;
+    cudaError_t get() {
+        std::lock_guard<std::mutex> l(g_stage_mu);
+        if (!g_stage_free.empty()) {
+            p = g_stage_free.back();
+            g_stage_free.pop_back();
+            return cudaSuccess;
+        }
+        return cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(Staging));
+    }
+    ~StagingLease() {
+        if (!p) return;
+        std::lock_guard<std::mutex> l(g_stage_mu);
+        g_stage_free.push_back(p);
+    }
+};
+}  // namespace
 
 int build_index(Index* ix, const double* X) {
     cudaStream_t s = ix->stream;
@@ -679,17 +712,12 @@ int build_index(Index* ix, const double* X) {
     if ((rc = col_reduce(X, m, step, n, kSum, nullptr, mean, nullptr, s))) return rc;
     if ((rc = col_reduce(X, m, step, n, kSqDev, mean, M->var, nullptr, s))) return rc;
     GJ_CUDA(cudaFreeAsync(mean, s));
-    // 2. permutation + geometry
+    // 2. permutation + geometry (read back with the cell count, step 6: nothing
+    // before needs it on the host)
     k_meta<<<1, 128, 0, s>>>(M, n, k, ix->eps, ix->opt.reorder); count_launch();
     GJ_CUDA(cudaGetLastError());
-    GJ_CUDA(cudaMemcpyAsync(&ix->h_meta, M, sizeof(Meta), cudaMemcpyDeviceToHost, s));
-    GJ_CUDA(cudaStreamSynchronize(s));
-    if (ix->h_meta.overflow) {
-        set_error("linearized cell id needs >= 2^63 cells (prod of per-dim widths); choose a smaller k");
-        return GJ_ERR_OVERFLOW;
-    }
-    const bool fp32_ok = fp32_threshold(ix);
-    const bool want32 = ix->filter >= 1 && fp32_ok;
+    StagingLease stage;
+    GJ_CUDA(stage.get());
     // 3. keys
     uint64_t *cellkey = nullptr, *ukey = nullptr, *tmp64 = nullptr;
     uint32_t* idx = nullptr;
@@ -715,18 +743,6 @@ int build_index(Index* ix, const double* X) {
     k_gather_points<<<(unsigned)std::min<int64_t>(blocks_for(N * 32, 256), 148 * 16), 256, 0, s>>>(X, idx, N, n, ix->n_pad, M,
                                                                                              ix->pts, nullptr); count_launch();
     GJ_CUDA(cudaMemcpyAsync(ix->orig, idx, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    if (ix->filter >= 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
-        bool tc_ok = false;
-        if ((rc = make_fp16(ix, &tc_ok))) return rc;
-        if (!tc_ok) ix->filter = want32 ? 1 : 0;
-    } else if (ix->filter == 1 && !want32) {
-        ix->filter = 0;
-    }
-    if (ix->filter == 1) {   // the FP32 filter's operands fl32(x - min), only when it runs
-        GJ_CUDA(pool_malloc(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
-        k_make32<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(ix->pts, N, n, ix->n_pad, M, ix->pts32); count_launch();
-        GJ_CUDA(cudaGetLastError());
-    }
     // 6. non-empty cells
     uint32_t *head = nullptr, *pos = nullptr, *d_tot = nullptr;
     GJ_CUDA(pool_malloc(&head, N * sizeof(uint32_t), s));
@@ -734,9 +750,25 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(pool_malloc(&d_tot, 4 * sizeof(uint32_t), s));
     k_heads<<<blocks_for(N, 256), 256, 0, s>>>(tmp64, N, head); count_launch();
     if ((rc = scan_u32(head, pos, N, d_tot, s))) return rc;
-    uint32_t h_tot = 0;
-    GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaMemcpyAsync(&stage.p->meta, M, sizeof(Meta), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaMemcpyAsync(&stage.p->count, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     GJ_CUDA(cudaStreamSynchronize(s));
+    ix->h_meta = stage.p->meta;
+    uint32_t h_tot = stage.p->count;
+    if (ix->h_meta.overflow) {
+        set_error("linearized cell id needs >= 2^63 cells (prod of per-dim widths); choose a smaller k");
+        return GJ_ERR_OVERFLOW;
+    }
+    const bool fp32_ok = fp32_threshold(ix);
+    const bool want32 = ix->filter >= 1 && fp32_ok;
+    // certified tensor-core operands (filter 2): launched here, R2 read back
+    // with the adjacency count below
+    unsigned long long* d_r2 = nullptr;
+    bool tc_launched = false;
+    if (ix->filter >= 2) {
+        GJ_CUDA(pool_malloc(&d_r2, sizeof(*d_r2), s));
+        if ((rc = make_fp16(ix, d_r2, &tc_launched))) return rc;
+    }
     const int64_t G = h_tot;
     ix->G = G;
     GJ_CUDA(pool_malloc(&ix->cell_id, G * sizeof(uint64_t), s));
@@ -754,9 +786,23 @@ int build_index(Index* ix, const double* X) {
     GJ_CUDA(cudaGetLastError());
     if ((rc = scan_u32(cnt, ix->nbr_off, G, d_tot, s))) return rc;
     GJ_CUDA(cudaMemcpyAsync(ix->nbr_off + G, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaMemcpyAsync(&stage.p->count, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    if (d_r2) GJ_CUDA(cudaMemcpyAsync(&stage.p->r2, d_r2, sizeof(*d_r2), cudaMemcpyDeviceToHost, s));
     GJ_CUDA(cudaStreamSynchronize(s));
-    ix->A = h_tot;
+    ix->A = stage.p->count;
+    if (ix->filter >= 2) {   // certified tensor-core bound, else fall back to the FP32 / FP64 scan
+        bool tc_ok = false;
+        if (tc_launched && (rc = make_fp16_finish(ix, stage.p->r2, &tc_ok))) return rc;
+        if (d_r2) GJ_CUDA(cudaFreeAsync(d_r2, s));
+        if (!tc_ok) ix->filter = want32 ? 1 : 0;
+    } else if (ix->filter == 1 && !want32) {
+        ix->filter = 0;
+    }
+    if (ix->filter == 1) {   // the FP32 filter's operands fl32(x - min), only when it runs
+        GJ_CUDA(pool_malloc(&ix->pts32, (size_t)N * ix->n_pad * sizeof(float), s));
+        k_make32<<<blocks_for(N * ix->n_pad, 256), 256, 0, s>>>(ix->pts, N, n, ix->n_pad, M, ix->pts32); count_launch();
+        GJ_CUDA(cudaGetLastError());
+    }
     GJ_CUDA(pool_malloc(&ix->nbr, std::max<int64_t>(1, ix->A) * sizeof(uint32_t), s));
     k_adjacent<true><<<blocks_for(G * 32, 256), 256, 0, s>>>(ix->cell_id, ix->cell_start, G, k, M, nullptr,
                                                             nullptr, nullptr, ix->nbr_off, ix->nbr, ix->nbr_self); count_launch();
@@ -765,9 +811,9 @@ int build_index(Index* ix, const double* X) {
     ix->tile_q = ix->filter == 2 ? 128 * (ix->opt.mma_tiles == 2 ? 2 : 1) : kTileQ;
     k_tile_count<<<blocks_for(G, 256), 256, 0, s>>>(ix->cell_start, G, (uint32_t)ix->tile_q, pos); count_launch();
     if ((rc = scan_u32(pos, pos, G, d_tot, s))) return rc;
-    GJ_CUDA(cudaMemcpyAsync(&h_tot, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    GJ_CUDA(cudaMemcpyAsync(&stage.p->count, d_tot, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     GJ_CUDA(cudaStreamSynchronize(s));
-    const int64_t T = h_tot;
+    const int64_t T = stage.p->count;
     ix->T = T;
     GJ_CUDA(pool_malloc(&ix->tile_cell, T * sizeof(uint32_t), s));
     GJ_CUDA(pool_malloc(&ix->tile_q0, T * sizeof(uint32_t), s));
