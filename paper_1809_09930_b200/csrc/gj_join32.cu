@@ -41,8 +41,17 @@ __device__ __forceinline__ double dist2_fp64(const double* __restrict__ a, const
     return acc;
 }
 
+// CTAs per SM the register allocation must allow for n > 64 (GJ_J32_MINB):
+// the 90-dim Songs-shaped query held in registers took 166 of them, leaving 3
+// CTAs (12 warps, 18 % warps active, 42 % of stalls at CTA barriers) per SM;
+// capped at 128 (4 CTAs, ~28 bytes of spills) the songs90 join went from 17.3
+// to 13.4 ms, at 96 (5 CTAs, 128 bytes of spills) to 18.6
+// (profiles/r2_ab_join32_registers.txt)
+#ifndef GJ_J32_MINB
+#define GJ_J32_MINB 4
+#endif
 template <int NPR, int MODE, bool SYM>
-__global__ void __launch_bounds__(kTileQ) k_join32(JoinParams P, JoinArgs A) {
+__global__ void __launch_bounds__(kTileQ, NPR >= 96 ? GJ_J32_MINB : 1) k_join32(JoinParams P, JoinArgs A) {
     constexpr int TC = (kSmemFloats / NPR) & ~1;   // candidates per stage (even: staged in pairs)
     __shared__ __align__(16) float Cs[kSmemFloats];
     __shared__ uint32_t Cid[TC];

@@ -19,5 +19,5 @@ timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --workload ex
 python bench.py --profile --steps 1 --warmup 1 > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_join_umma -s 5 -c 3 -o gpurun_out/join \
+ncu --set full --clock-control none --import-source on -k regex:k_join_umma -s 6 -c 3 -o gpurun_out/join \
     python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_join.log 2>&1
