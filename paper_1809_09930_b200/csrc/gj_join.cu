@@ -431,13 +431,19 @@ static bool plan_parts(const Index* ix, const JoinArgs& a, std::vector<uint32_t>
         W += w;
         wmax = w > wmax ? w : wmax;
     }
-    // parts of about 1 / (148 x div) of the launch's work (div = 8; GJ_PLAN_DIV
-    // overrides it for timing experiments, read once)
-    static const double div = [] {
+    // parts of about 1 / (148 x div) of the launch's work: div = 4 for the
+    // tcgen05 kernels, whose persistent CTAs take items from a counter (coarse
+    // first parts, the guided sizing below refines the tail; expo32 8-rank
+    // projection 0.84-0.85 vs 0.83-0.84 with 8), div = 8 for the SIMT kernels
+    // whose CTAs are dispatched once per item (songs90 FP32 join 13.4 ms vs 17.9
+    // with 4; profiles/r2_ab_plan_div_persistent.txt).  GJ_PLAN_DIV overrides
+    // both (timing experiments, read once).
+    static const double env_div = [] {
         const char* e = getenv("GJ_PLAN_DIV");
         const double v = e ? atof(e) : 0.0;
-        return v > 0.0 ? v : 8.0;
+        return v > 0.0 ? v : 0.0;
     }();
+    const double div = env_div > 0.0 ? env_div : (ix->filter == 2 ? 4.0 : 8.0);
     const double target = W / (148.0 * div);
     if (!(target > 0.0) || wmax <= target) return false;
     // Guided self-scheduling (items are taken in order: the persistent tcgen05
