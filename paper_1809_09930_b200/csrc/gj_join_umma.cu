@@ -621,8 +621,12 @@ int launch_umma_k(const JoinParams& p, const JoinArgs& a, cudaStream_t s) {
     uint32_t* counter = nullptr;
     unsigned grid = total;
     if (MT == 1) {   // persistent CTAs: as many as fit, items from an atomic counter
-        static int n_sm = 0;
-        if (!n_sm) GJ_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        static std::atomic<int> sms{0};   // SM count of this device (148 on B200); racing first calls agree
+        int n_sm = sms.load();
+        if (!n_sm) {
+            GJ_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+            sms.store(n_sm);
+        }
         grid = std::min<unsigned>(total, (unsigned)(n_sm * kCtas));
         GJ_CUDA(pool_malloc(&counter, sizeof(uint32_t), s));
         GJ_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
